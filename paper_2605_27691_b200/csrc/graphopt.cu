@@ -1,0 +1,275 @@
+// graphopt.cu -- optimize_graph (graphopt.cpp:24-105) on the B200.
+//
+//   k_prune     CTA per row: the row's k neighbor vectors are staged in smem
+//               (cp.async), all k(k-1)/2 exact-order distances are computed
+//               with 4x4 register micro-tiles, giving a detour bitmask per
+//               rank; the kept set is the sequential scan of pass 1
+//               (:35-58) done on bitmasks.  Same kept set as the reference's
+//               early-exit loop because the predicate is evaluated exactly.
+//   scan + k_rev_fill   reverse edges of kept forward edges as a CSR of packed
+//               (dist, src) keys -- the serial aggregation at :60-69.
+//   k_fill      warp per row: pass 2 (:77-103): kept forward, then reverse by
+//               ascending (dist, src) skipping self and duplicates, then
+//               pruned forward; exactly out_degree ids.
+#include "graphopt.hpp"
+
+namespace knng_b200 {
+namespace {
+
+constexpr int kPruneThreads = 64;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+struct PruneArgs {
+  const u64* keys;  // n x k packed rows
+  u64 n;
+  u32 k;
+  u32 id_base;  // ids in keys are (local id + id_base)
+  const float* X;
+  int d;
+  int DC, DCP;
+  u32* kept;   // n bitmasks
+  u32* rcnt;   // n reverse-edge counts
+};
+
+__global__ __launch_bounds__(kPruneThreads) void k_prune(PruneArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  u32* s_ids = reinterpret_cast<u32*>(smem);          // 32
+  float* s_d = reinterpret_cast<float*>(smem + 128);  // 32
+  u32* s_det = reinterpret_cast<u32*>(smem + 256);    // 32
+  float* s_x = reinterpret_cast<float*>(smem + 384);
+  const int tid = threadIdx.x;
+  const int k = (int)a.k;
+  const int RT = (k + 3) >> 2;
+  const int ntiles = RT * RT;
+  const bool vec = (a.d & 3) == 0;
+  for (u64 u = blockIdx.x; u < a.n; u += gridDim.x) {
+    __syncthreads();
+    if (tid < 32) {
+      if (tid < k) {
+        const u64 key = a.keys[u * k + tid];
+        s_ids[tid] = key_id(key) - a.id_base;
+        s_d[tid] = key_dist(key);
+      }
+      s_det[tid] = 0;
+    }
+    float acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+    const int ti = tid / RT, tj = tid - ti * RT;
+    const bool active = tid < ntiles;
+    for (int c0 = 0; c0 < a.d; c0 += a.DC) {
+      const int dc = min(a.DC, a.d - c0);
+      __syncthreads();
+      if (vec) {
+        const int q = dc >> 2;
+        for (int t = tid; t < k * q; t += kPruneThreads) {
+          const int row = t / q, c4 = t - row * q;
+          cp_async16(s_x + row * a.DCP + c4 * 4, a.X + (u64)s_ids[row] * a.d + c0 + c4 * 4);
+        }
+        cp_async_wait_all();
+      } else {
+        for (int t = tid; t < k * dc; t += kPruneThreads) {
+          const int row = t / dc, c = t - row * dc;
+          s_x[row * a.DCP + c] = a.X[(u64)s_ids[row] * a.d + c0 + c];
+        }
+      }
+      __syncthreads();
+      if (active) {
+        const float* ra[4];
+        const float* rb[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) ra[r] = s_x + (ti + RT * r) * a.DCP;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rb[c] = s_x + (tj + RT * c) * a.DCP;
+        const int dc4 = dc & ~3;
+        for (int dd = 0; dd < dc4; dd += 4) {
+          float4 va[4], vb[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) va[r] = *reinterpret_cast<const float4*>(ra[r] + dd);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) vb[c] = *reinterpret_cast<const float4*>(rb[c] + dd);
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[r][c] = sq_step4(acc[r][c], va[r], vb[c]);
+        }
+        for (int dd = dc4; dd < dc; ++dd) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[r][c] = sq_step(acc[r][c], ra[r][dd], rb[c][dd]);
+        }
+      }
+    }
+    // detour predicate sigma(v_i, w_j) < d[u->w_j] for i < j (graphopt.cpp:45-50)
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = ti + RT * r;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int j = tj + RT * c;
+          if (i < j && j < k && __fsqrt_rn(acc[r][c]) < s_d[j]) atomicOr(&s_det[j], 1u << i);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {
+      // sequential kept scan on bitmasks
+      u32 kept = 0;
+      for (int j = 0; j < k; ++j)
+        if ((s_det[j] & kept) == 0) kept |= 1u << j;
+      if (tid == 0) a.kept[u] = kept;
+      if (tid < k && ((kept >> tid) & 1u)) atomicAdd(&a.rcnt[s_ids[tid]], 1u);
+    }
+  }
+}
+
+__global__ __launch_bounds__(256) void k_rev_fill(const u64* __restrict__ keys, u64 n, u32 k,
+                                                  u32 id_base, const u32* __restrict__ kept,
+                                                  const u64* __restrict__ roff,
+                                                  u32* __restrict__ cur, u64* __restrict__ rbuf) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 u = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); u < n; u += warps) {
+    const u32 km = kept[u];
+    if (lane < k && ((km >> lane) & 1u)) {
+      const u64 key = keys[u * k + lane];
+      const u32 w = key_id(key) - id_base;
+      rbuf[roff[w] + atomicAdd(&cur[w], 1u)] = pack_key(key_dist(key), (u32)u);
+    }
+  }
+}
+
+__global__ __launch_bounds__(256) void k_fill(const u64* __restrict__ keys, u64 n, u32 k,
+                                              u32 id_base, u32 od, const u32* __restrict__ kept,
+                                              const u64* __restrict__ roff,
+                                              const u64* __restrict__ rbuf,
+                                              u32* __restrict__ sg) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 u = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); u < n; u += warps) {
+    const u32 km = kept[u];
+    const u32 id = lane < k ? key_id(keys[u * k + lane]) - id_base : 0xffffffffu;
+    const bool isk = (km >> lane) & 1u;
+    // row under construction: lane t holds row[t]
+    u32 row = 0xffffffffu;
+    u32 cnt = 0;
+    {
+      const u32 rank = __popc(km & lanemask_lt());
+      // scatter kept forward entries (in rank order) to lanes rank < od
+      for (u32 j = 0; j < k; ++j) {
+        const u32 v = __shfl_sync(kFull, id, j);
+        if (((km >> j) & 1u) && cnt < od) {
+          if (lane == cnt) row = v;
+          ++cnt;
+        }
+      }
+      (void)rank;
+      (void)isk;
+    }
+    if (cnt < od) {
+      // reverse candidates in ascending (dist, src) order (graphopt.cpp:87-93)
+      const u64 lo = roff[u], hi = roff[u + 1];
+      u64 prev = 0;
+      bool have_prev = false;
+      while (cnt < od) {
+        u64 best = kEmptyKey;
+        for (u64 t = lo + lane; t < hi; t += 32) {
+          const u64 c = rbuf[t];
+          if ((!have_prev || c > prev) && c < best) best = c;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const u64 other = __shfl_xor_sync(kFull, best, o);
+          best = other < best ? other : best;
+        }
+        if (best == kEmptyKey) break;
+        prev = best;
+        have_prev = true;
+        const u32 cid = key_id(best);
+        const bool dup = __ballot_sync(kFull, lane < cnt && row == cid) != 0;
+        if (cid != (u32)u && !dup) {
+          if (lane == cnt) row = cid;
+          ++cnt;
+        }
+      }
+    }
+    // pruned forward entries (graphopt.cpp:95-97)
+    for (u32 j = 0; j < k && cnt < od; ++j) {
+      if ((km >> j) & 1u) continue;
+      const u32 v = __shfl_sync(kFull, id, j);
+      const bool dup = __ballot_sync(kFull, lane < cnt && row == v) != 0;
+      if (!dup) {
+        if (lane == cnt) row = v;
+        ++cnt;
+      }
+    }
+    if (lane < od) sg[u * od + lane] = row;
+  }
+}
+
+unsigned warp_grid(const Runner& r, u64 items) {
+  const u64 want = ceil_div<u64>(items, 8);
+  const u64 cap = (u64)r.num_sms * 16;
+  return (unsigned)(want < cap ? (want ? want : 1) : cap);
+}
+
+}  // namespace
+
+void optimize_graph_device(Runner& r, const uint64_t* keys, uint64_t n, uint32_t k,
+                           uint32_t id_base, const float* X, int d, uint32_t out_degree,
+                           uint32_t* sg, uint64_t* launches) {
+  if (out_degree == 0) out_degree = k;
+  require(out_degree <= k, "optimize_graph: out_degree must be <= k");
+  require(k >= 1 && k <= 32, "optimize_graph: the B200 path supports 1 <= k <= 32");
+  if (n == 0) return;
+  DeviceGuard guard(r.device);
+  DBuf<u32> kept(r, n), rcnt(r, n);
+  DBuf<u64> roff(r, n + 1);
+  rcnt.zero();
+  PruneArgs a{};
+  a.keys = keys;
+  a.n = n;
+  a.k = k;
+  a.id_base = id_base;
+  a.X = X;
+  a.d = d;
+  a.DC = d <= 128 ? ((d + 7) & ~7) : 128;
+  a.DCP = a.DC + 4;
+  a.kept = kept.p;
+  a.rcnt = rcnt.p;
+  const int rows = ((int)k + 3) & ~3;
+  const size_t smem = 384 + (size_t)rows * a.DCP * 4;
+  KNNG_CUDA(cudaFuncSetAttribute(k_prune, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  int per_sm = 0;
+  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prune, kPruneThreads, smem));
+  if (per_sm < 1) per_sm = 1;
+  k_prune<<<persistent_grid(r, per_sm, n), kPruneThreads, smem, r.stream>>>(a);
+  KNNG_LAUNCH_CHECK();
+  exclusive_scan_u32(r, rcnt.p, roff.p, n);
+  uint64_t total = 0;
+  KNNG_CUDA(cudaMemcpyAsync(&total, roff.p + n, sizeof(u64), cudaMemcpyDeviceToHost, r.stream));
+  r.sync();
+  DBuf<u64> rbuf(r, total ? total : 1);
+  rcnt.zero();
+  k_rev_fill<<<warp_grid(r, n), 256, 0, r.stream>>>(keys, n, k, id_base, kept.p, roff.p, rcnt.p,
+                                                    rbuf.p);
+  KNNG_LAUNCH_CHECK();
+  k_fill<<<warp_grid(r, n), 256, 0, r.stream>>>(keys, n, k, id_base, out_degree, kept.p, roff.p,
+                                                rbuf.p, sg);
+  KNNG_LAUNCH_CHECK();
+  if (launches) *launches += 4 + 3;
+}
+
+}  // namespace knng_b200

@@ -1,0 +1,728 @@
+// nndescent.cu -- B200 lock-free NN-Descent (north_star item 2).
+//
+// Per iteration (nndescent.cpp:247-257):
+//   k_sample_fwd   warp per point: forward new/old samples, exactly the
+//                  reference's sampling stream (nndescent.cpp:80-104)
+//   scan + k_fill_rev + k_rev_select: the serial transpose (:108-113) as a
+//                  counting sort; each reverse list is ranked in ascending
+//                  source order and sampled with the reference's rng stream
+//                  (:114-127), so the sampled lists equal the reference's.
+//   k_join         CTA per point: dedup'd new/old lists (:135-153), feature
+//                  rows staged in smem with cp.async (16 B), 4x4 register
+//                  micro-tiles of exact-order distances, offers (:157-197)
+//                  resolved by 64-bit packed (dist,id) atomicMin into hashed
+//                  candidate slots -- lock-free, order-independent, so the
+//                  build is deterministic regardless of scheduling.
+//   k_apply        warp per point: knn_insert of every surviving slot in slot
+//                  order (:199-223), gross accepted count, worst refresh.
+#include <cmath>
+
+#include "nndescent.hpp"
+
+namespace knng_b200 {
+namespace {
+
+constexpr u32 kNone = 0xffffffffu;
+
+__device__ __forceinline__ u32 kmask_of(u32 k) { return k >= 32 ? kFull : ((1u << k) - 1u); }
+
+// Slot of candidate v in point u's hashed candidate buffer.
+__device__ __forceinline__ u32 slot_hash(u32 u, u32 v, u32 S) {
+  u32 x = v * 0x9E3779B1u + u * 0x85EBCA77u;
+  x ^= x >> 15;
+  x *= 0x2C1B3C6Du;
+  x ^= x >> 12;
+  x *= 0x297A2D39u;
+  x ^= x >> 15;
+  return x % S;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// init_random_graph nndescent.cpp:29-62 -- warp per row
+// ---------------------------------------------------------------------------
+__global__ __launch_bounds__(256) void k_init(const float* __restrict__ X, u64 n, int d, u32 k,
+                                              u64 seed, u64* __restrict__ keys,
+                                              u32* __restrict__ flags,
+                                              float* __restrict__ worst) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 r = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    Rng rng(mix_seed(seed, r));
+    u32 my_id = kNone;
+    u32 fill = 0;
+    while (fill < k) {
+      u32 id = (u32)rng.next_below(n - 1);
+      if (id >= r) ++id;
+      const bool dup = __ballot_sync(kFull, lane < fill && my_id == id) != 0;
+      if (dup) continue;
+      if (lane == fill) my_id = id;
+      ++fill;
+    }
+    u64 key = kEmptyKey;
+    if (lane < k) key = pack_key(l2_exact(X + r * d, X + (u64)my_id * d, d), my_id);
+    key = warp_sort32(key);
+    if (lane < k) keys[r * k + lane] = key;
+    const u64 last = __shfl_sync(kFull, key, k - 1);
+    if (lane == 0) {
+      flags[r] = kmask_of(k);
+      worst[r] = key_dist(last);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sample_neighbors, forward half (nndescent.cpp:80-104) -- warp per point
+// ---------------------------------------------------------------------------
+__global__ __launch_bounds__(256) void k_sample_fwd(const u64* __restrict__ keys,
+                                                    u32* __restrict__ flags, u64 n, u32 k,
+                                                    u32 B, u64 iter_seed, u32* __restrict__ nf,
+                                                    u32* __restrict__ nfn, u32* __restrict__ of,
+                                                    u32* __restrict__ ofn,
+                                                    u32* __restrict__ cnt_new,
+                                                    u32* __restrict__ cnt_old) {
+  const unsigned lane = lane_id();
+  const u32 km = kmask_of(k);
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); p < n; p += warps) {
+    const u32 id = lane < k ? key_id(keys[p * k + lane]) : kNone;
+    const u32 fm = flags[p] & km;
+    const bool isnew = (fm >> lane) & 1u;
+    const u32 np = __popc(fm);
+    const unsigned lt = lanemask_lt();
+    if (lane < k && !isnew) {
+      of[p * k + __popc(~fm & km & lt)] = id;
+      atomicAdd(&cnt_old[id], 1u);
+    }
+    if (np <= B) {
+      if (isnew) {
+        nf[p * B + __popc(fm & lt)] = id;
+        atomicAdd(&cnt_new[id], 1u);
+      }
+      if (lane == 0) {
+        nfn[p] = np;
+        ofn[p] = k - np;
+        flags[p] = 0;
+      }
+    } else {
+      // sample_distinct(np, B, Rng(mix_seed(iter_seed, p))) rng.hpp:66-87
+      Rng rng(mix_seed(iter_seed, p));
+      u32 picked = 0, my_pick = kNone;
+      for (u32 cnt = 0; cnt < B;) {
+        const u32 x = (u32)rng.next_below(np);
+        if ((picked >> x) & 1u) continue;
+        picked |= 1u << x;
+        if (lane == cnt) my_pick = x;
+        ++cnt;
+      }
+      const u32 rank = isnew ? __popc(fm & lt) : kNone;
+      u32 cleared = 0;
+      for (u32 i = 0; i < B; ++i) {
+        const u32 pi = __shfl_sync(kFull, my_pick, i);
+        const unsigned b = __ballot_sync(kFull, rank == pi);
+        const int src = __ffs(b) - 1;
+        if ((int)lane == src) {
+          nf[p * B + i] = id;
+          atomicAdd(&cnt_new[id], 1u);
+        }
+        cleared |= b;
+      }
+      if (lane == 0) {
+        nfn[p] = B;
+        ofn[p] = k - np;
+        flags[p] = fm & ~cleared;
+      }
+    }
+  }
+}
+
+// Reverse lists: append p to the CSR segment of every forward target.
+__global__ __launch_bounds__(256) void k_fill_rev(u64 n, u32 k, u32 B, const u32* __restrict__ nf,
+                                                  const u32* __restrict__ nfn,
+                                                  const u32* __restrict__ of,
+                                                  const u32* __restrict__ ofn,
+                                                  const u64* __restrict__ off_new,
+                                                  const u64* __restrict__ off_old,
+                                                  u32* __restrict__ cur_new,
+                                                  u32* __restrict__ cur_old,
+                                                  u32* __restrict__ buf_new,
+                                                  u32* __restrict__ buf_old) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); p < n; p += warps) {
+    if (lane < nfn[p]) {
+      const u32 id = nf[p * B + lane];
+      buf_new[off_new[id] + atomicAdd(&cur_new[id], 1u)] = (u32)p;
+    }
+    if (lane < ofn[p]) {
+      const u32 id = of[p * k + lane];
+      buf_old[off_old[id] + atomicAdd(&cur_old[id], 1u)] = (u32)p;
+    }
+  }
+}
+
+// Reverse sampling nndescent.cpp:114-127: the segment of v, ranked in
+// ascending source order (= the serial transpose order), sampled with
+// Rng(mix_seed(iter_seed, 2^63|v)) shared by new_rev then old_rev.
+__global__ __launch_bounds__(256) void k_rev_select(u64 n, u32 B, u64 iter_seed,
+                                                    const u64* __restrict__ off_new,
+                                                    const u32* __restrict__ buf_new,
+                                                    const u64* __restrict__ off_old,
+                                                    const u32* __restrict__ buf_old,
+                                                    u32* __restrict__ nr, u32* __restrict__ nrn,
+                                                    u32* __restrict__ orv,
+                                                    u32* __restrict__ orn) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 v = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); v < n; v += warps) {
+    Rng rng(mix_seed(iter_seed, 0x8000000000000000ull | v));
+    for (int which = 0; which < 2; ++which) {
+      const u64* off = which ? off_old : off_new;
+      const u32* buf = which ? buf_old : buf_new;
+      u32* out = (which ? orv : nr) + v * B;
+      u32* outn = which ? orn : nrn;
+      const u64 lo = off[v];
+      const u32 len = (u32)(off[v + 1] - lo);
+      const u32* seg = buf + lo;
+      if (len <= B) {
+        u64 e = lane < len ? (u64)seg[lane] : kEmptyKey;
+        e = warp_sort32(e);
+        if (lane < len) out[lane] = (u32)e;
+        if (lane == 0) outn[v] = len;
+        continue;
+      }
+      u32 my_pick = kNone;
+      for (u32 cnt = 0; cnt < B;) {
+        const u32 x = (u32)rng.next_below(len);
+        if (__ballot_sync(kFull, lane < cnt && my_pick == x)) continue;
+        if (lane == cnt) my_pick = x;
+        ++cnt;
+      }
+      for (u32 base = 0; base < len; base += 32) {
+        const u32 idx = base + lane;
+        const u32 e = idx < len ? seg[idx] : kNone;
+        u32 rank = 0;
+        for (u32 j = 0; j < len; ++j) rank += (seg[j] < e) ? 1u : 0u;
+        if (idx >= len) rank = kNone;
+        for (u32 i = 0; i < B; ++i) {
+          const u32 pi = __shfl_sync(kFull, my_pick, i);
+          if (rank == pi) out[i] = e;
+        }
+      }
+      if (lane == 0) outn[v] = B;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// local_join nndescent.cpp:135-197 -- CTA per point
+// ---------------------------------------------------------------------------
+constexpr int kJoinThreads = 128;
+constexpr int kTPT = 2;  // micro-tiles per thread per pass
+
+struct JoinArgs {
+  const float* X;
+  u64 n;
+  int d;
+  u32 k;
+  u32 B;
+  const u32 *nf, *nfn, *of, *ofn, *nr, *nrn, *orv, *orn;
+  const float* worst;
+  u64* slots;
+  u32 S;
+  u64* counters;
+  int DC;    // dims per staged chunk (multiple of 8)
+  int DCP;   // smem row stride in floats (DCP/4 odd: conflict-free LDS.128)
+  int RMAX;  // smem rows (>= max list size, multiple of 4)
+};
+
+// Append the unique, not-yet-listed ids of src[0..len) to s_ids[*cnt..).
+__device__ __forceinline__ void warp_append_unique(u32* s_ids, int& cnt, const u32* src,
+                                                   u32 len) {
+  const unsigned lane = lane_id();
+  for (u32 base = 0; base < len; base += 32) {
+    const bool valid = base + lane < len;
+    const u32 c = valid ? src[base + lane] : kNone;
+    const unsigned m = __match_any_sync(kFull, c);
+    bool keep = valid && (__ffs(m) - 1 == (int)lane);
+    for (int t = 0; t < cnt; ++t) keep = keep && (s_ids[t] != c);
+    const unsigned b = __ballot_sync(kFull, keep);
+    if (keep) s_ids[cnt + __popc(b & lanemask_lt())] = c;
+    cnt += __popc(b);
+    __syncwarp();
+  }
+}
+
+__global__ __launch_bounds__(kJoinThreads) void k_join(JoinArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  u32* s_ids = reinterpret_cast<u32*>(smem);
+  int* s_cnt = reinterpret_cast<int*>(smem + a.RMAX * 4);
+  float* s_x = reinterpret_cast<float*>(smem + a.RMAX * 4 + 16);
+  const int tid = threadIdx.x;
+  const unsigned lane = lane_id();
+  const bool vec = (a.d & 3) == 0;
+  u64 my_pairs = 0, my_offers = 0, my_rows = 0, my_pts = 0;
+
+  for (u64 p = blockIdx.x; p < a.n; p += gridDim.x) {
+    __syncthreads();  // previous point's smem fully consumed
+    if (tid < 32) {
+      int nn = 0;
+      warp_append_unique(s_ids, nn, a.nf + p * a.B, a.nfn[p]);
+      warp_append_unique(s_ids, nn, a.nr + p * a.B, a.nrn[p]);
+      int na = nn;
+      warp_append_unique(s_ids, na, a.of + p * a.k, a.ofn[p]);
+      warp_append_unique(s_ids, na, a.orv + p * a.B, a.orn[p]);
+      if (lane == 0) {
+        s_cnt[0] = nn;
+        s_cnt[1] = na;
+      }
+    }
+    __syncthreads();
+    const int nn = s_cnt[0], na = s_cnt[1];
+    if (nn == 0 || na < 2) continue;
+    const int RT = (nn + 3) >> 2, CT = (na + 3) >> 2;
+    const int ntiles = RT * CT;
+    if (tid == 0) {
+      ++my_pts;
+      my_rows += (u64)na;
+    }
+    for (int pass = 0; pass < ntiles; pass += kJoinThreads * kTPT) {
+      float acc[kTPT][4][4];
+#pragma unroll
+      for (int m = 0; m < kTPT; ++m)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[m][r][c] = 0.0f;
+      for (int c0 = 0; c0 < a.d; c0 += a.DC) {
+        const int dc = min(a.DC, a.d - c0);
+        __syncthreads();
+        if (vec) {
+          const int q = dc >> 2;
+          for (int t = tid; t < na * q; t += kJoinThreads) {
+            const int row = t / q, c4 = t - row * q;
+            cp_async16(s_x + row * a.DCP + c4 * 4,
+                       a.X + (u64)s_ids[row] * a.d + c0 + c4 * 4);
+          }
+          cp_async_wait_all();
+        } else {
+          for (int t = tid; t < na * dc; t += kJoinThreads) {
+            const int row = t / dc, c = t - row * dc;
+            s_x[row * a.DCP + c] = a.X[(u64)s_ids[row] * a.d + c0 + c];
+          }
+        }
+        __syncthreads();
+        const int dc4 = dc & ~3;
+#pragma unroll
+        for (int m = 0; m < kTPT; ++m) {
+          const int t = pass + tid + m * kJoinThreads;
+          if (t >= ntiles) continue;
+          const int ti = t / CT, tj = t - ti * CT;
+          const float* ra[4];
+          const float* rb[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) ra[r] = s_x + (ti + RT * r) * a.DCP;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) rb[c] = s_x + (tj + CT * c) * a.DCP;
+          for (int dd = 0; dd < dc4; dd += 4) {
+            float4 va[4], vb[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) va[r] = *reinterpret_cast<const float4*>(ra[r] + dd);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) vb[c] = *reinterpret_cast<const float4*>(rb[c] + dd);
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) acc[m][r][c] = sq_step4(acc[m][r][c], va[r], vb[c]);
+          }
+          for (int dd = dc4; dd < dc; ++dd) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) acc[m][r][c] = sq_step(acc[m][r][c], ra[r][dd], rb[c][dd]);
+          }
+        }
+      }
+      // offers: (u, v, sigma) to both endpoints (nndescent.cpp:160-171)
+#pragma unroll
+      for (int m = 0; m < kTPT; ++m) {
+        const int t = pass + tid + m * kJoinThreads;
+        if (t >= ntiles) continue;
+        const int ti = t / CT, tj = t - ti * CT;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = ti + RT * r;
+          if (i >= nn) continue;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int j = tj + CT * c;
+            if (j >= na || j <= i) continue;
+            const u32 u = s_ids[i], v = s_ids[j];
+            const float dist = __fsqrt_rn(acc[m][r][c]);
+            ++my_pairs;
+            if (dist < a.worst[u]) {
+              atomicMin(reinterpret_cast<unsigned long long*>(a.slots + (u64)u * a.S +
+                                                              slot_hash(u, v, a.S)),
+                        (unsigned long long)pack_key(dist, v));
+              ++my_offers;
+            }
+            if (dist < a.worst[v]) {
+              atomicMin(reinterpret_cast<unsigned long long*>(a.slots + (u64)v * a.S +
+                                                              slot_hash(v, u, a.S)),
+                        (unsigned long long)pack_key(dist, u));
+              ++my_offers;
+            }
+          }
+        }
+      }
+    }
+  }
+  // one atomic per warp for the device counters
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    my_pairs += __shfl_xor_sync(kFull, my_pairs, o);
+    my_offers += __shfl_xor_sync(kFull, my_offers, o);
+  }
+  if (lane == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntPairs), my_pairs);
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntOffers), my_offers);
+  }
+  if (tid == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntStagedRows), my_rows);
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntJoinPoints), my_pts);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// apply_candidates nndescent.cpp:199-223 -- warp per point
+// ---------------------------------------------------------------------------
+__global__ __launch_bounds__(256) void k_apply(u64 n, u32 k, u32 S, u64* __restrict__ keys,
+                                               u32* __restrict__ flags,
+                                               float* __restrict__ worst,
+                                               u64* __restrict__ slots,
+                                               u64* __restrict__ counters) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  u64 acc_total = 0;
+  for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); p < n; p += warps) {
+    u64* sl = slots + p * S;
+    // cheap skip: any slot filled?
+    u64 rk = kEmptyKey;
+    bool loaded = false;
+    u32 fl = 0, accepted = 0;
+    u64 last = 0;
+    for (u32 c0 = 0; c0 < S; c0 += 32) {
+      const u32 si = c0 + lane;
+      const u64 s = si < S ? sl[si] : kEmptyKey;
+      const bool filled = s != kEmptyKey;
+      if (filled) sl[si] = kEmptyKey;  // CandidateBuffer::reset
+      unsigned mask = __ballot_sync(kFull, filled);
+      if (!mask) continue;
+      if (!loaded) {
+        loaded = true;
+        rk = lane < k ? keys[p * k + lane] : kEmptyKey;
+        fl = (flags[p] >> lane) & 1u;
+        last = __shfl_sync(kFull, rk, k - 1);
+      }
+      mask = __ballot_sync(kFull, filled && s < last);
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const u64 c = __shfl_sync(kFull, s, src);
+        // knn_insert core.cpp:99-112: reject duplicates and non-improvements
+        if (c >= last) continue;
+        if (__ballot_sync(kFull, lane < k && key_id(rk) == key_id(c))) continue;
+        const u32 pos = __popc(__ballot_sync(kFull, lane < k && rk < c));
+        const u64 up = __shfl_up_sync(kFull, rk, 1);
+        const u32 upf = __shfl_up_sync(kFull, fl, 1);
+        if (lane > pos && lane < k) {
+          rk = up;
+          fl = upf;
+        }
+        if (lane == pos) {
+          rk = c;
+          fl = 1;
+        }
+        last = __shfl_sync(kFull, rk, k - 1);
+        ++accepted;
+      }
+    }
+    if (accepted) {
+      if (lane < k) keys[p * k + lane] = rk;
+      const unsigned fmask = __ballot_sync(kFull, fl && lane < k);
+      if (lane == 0) {
+        flags[p] = fmask;
+        worst[p] = key_dist(last);
+      }
+      acc_total += accepted;
+    }
+  }
+  if (lane == 0 && acc_total)
+    atomicAdd(reinterpret_cast<unsigned long long*>(counters + kCntAccepted), acc_total);
+}
+
+// ---------------------------------------------------------------------------
+// layout conversion
+// ---------------------------------------------------------------------------
+__global__ void k_export(const u64* __restrict__ keys, const u32* __restrict__ flags, u64 n,
+                         u32 k, u32 shift, u32* __restrict__ ids, float* __restrict__ dists,
+                         uint8_t* __restrict__ f8) {
+  const u64 total = n * k;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (u64)gridDim.x * blockDim.x) {
+    const u64 key = keys[i];
+    if (ids) ids[i] = key_id(key) + shift;
+    if (dists) dists[i] = key_dist(key);
+    if (f8) f8[i] = flags ? (uint8_t)((flags[i / k] >> (i % k)) & 1u) : 0;
+  }
+}
+
+__global__ __launch_bounds__(256) void k_import(const u32* __restrict__ ids,
+                                                const float* __restrict__ dists,
+                                                const uint8_t* __restrict__ f8, u64 n, u32 k,
+                                                u64* __restrict__ keys,
+                                                u32* __restrict__ flags) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 r = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    bool f = false;
+    if (lane < k) {
+      keys[r * k + lane] = pack_key(dists[r * k + lane], ids[r * k + lane]);
+      f = f8 ? f8[r * k + lane] != 0 : false;
+    }
+    const unsigned m = __ballot_sync(kFull, f);
+    if (flags && lane == 0) flags[r] = m;
+  }
+}
+
+unsigned warp_grid(const Runner& r, u64 items) {
+  const u64 want = ceil_div<u64>(items, 8);
+  const u64 cap = (u64)r.num_sms * 16;
+  return (unsigned)(want < cap ? (want ? want : 1) : cap);
+}
+
+uint32_t bound_of(double rho, uint32_t k) {
+  return (uint32_t)std::ceil(rho * (double)k);
+}
+
+}  // namespace
+
+void validate_nnd(const NndParams& p, uint64_t n) {
+  require(!(p.rho <= 0.0 || p.rho > 1.0), "nn_descent: rho must be in (0, 1]");
+  require(p.delta >= 0.0, "nn_descent: delta must be >= 0");
+  const uint64_t cap = p.candidate_capacity ? p.candidate_capacity : 2ull * p.k;
+  require(cap >= p.k, "nn_descent: candidate_capacity must be >= k");
+  require(p.k >= 1 && p.k < n, "init_random_graph: need 1 <= k < N");
+  require(p.k <= 32, "nn_descent: the B200 path supports k <= 32");
+  require(n < 0xffffffffull, "nn_descent: N must fit a 32-bit point id");
+}
+
+void init_random_graph_device(Runner& r, const DevRows& ds, uint32_t k, uint64_t seed,
+                              uint64_t* keys, uint32_t* flags) {
+  require(k >= 1 && k < ds.n, "init_random_graph: need 1 <= k < N");
+  require(k <= 32, "init_random_graph: the B200 path supports k <= 32");
+  DBuf<float> worst(r, ds.n);
+  k_init<<<warp_grid(r, ds.n), 256, 0, r.stream>>>(ds.x, ds.n, ds.d, k, seed, keys, flags,
+                                                   worst.p);
+  KNNG_LAUNCH_CHECK();
+}
+
+namespace {
+
+struct RevCsr {
+  DBuf<u32> cnt_new, cnt_old;
+  DBuf<u64> off_new, off_old;
+  DBuf<u32> buf_new, buf_old;
+};
+
+void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_seed,
+                 const uint64_t* keys, uint32_t* flags, SampleLists& s, RevCsr& c,
+                 uint64_t* launches) {
+  const unsigned g = warp_grid(r, n);
+  c.cnt_new.zero();
+  c.cnt_old.zero();
+  k_sample_fwd<<<g, 256, 0, r.stream>>>(keys, flags, n, k, B, iter_seed, s.nf.p, s.nfn.p,
+                                        s.of.p, s.ofn.p, c.cnt_new.p, c.cnt_old.p);
+  KNNG_LAUNCH_CHECK();
+  exclusive_scan_u32(r, c.cnt_new.p, c.off_new.p, n);
+  exclusive_scan_u32(r, c.cnt_old.p, c.off_old.p, n);
+  c.cnt_new.zero();
+  c.cnt_old.zero();
+  k_fill_rev<<<g, 256, 0, r.stream>>>(n, k, B, s.nf.p, s.nfn.p, s.of.p, s.ofn.p, c.off_new.p,
+                                      c.off_old.p, c.cnt_new.p, c.cnt_old.p, c.buf_new.p,
+                                      c.buf_old.p);
+  KNNG_LAUNCH_CHECK();
+  k_rev_select<<<g, 256, 0, r.stream>>>(n, B, iter_seed, c.off_new.p, c.buf_new.p, c.off_old.p,
+                                        c.buf_old.p, s.nr.p, s.nrn.p, s.orv.p, s.orn.p);
+  KNNG_LAUNCH_CHECK();
+  if (launches) *launches += 3 + 2 * 3;
+}
+
+void alloc_lists(Runner& r, uint64_t n, uint32_t k, uint32_t B, SampleLists& s, RevCsr& c) {
+  s.bound = B;
+  const u64 b = B ? B : 1;
+  s.nf.alloc(r, n * b);
+  s.nfn.alloc(r, n);
+  s.of.alloc(r, n * k);
+  s.ofn.alloc(r, n);
+  s.nr.alloc(r, n * b);
+  s.nrn.alloc(r, n);
+  s.orv.alloc(r, n * b);
+  s.orn.alloc(r, n);
+  c.cnt_new.alloc(r, n);
+  c.cnt_old.alloc(r, n);
+  c.off_new.alloc(r, n + 1);
+  c.off_old.alloc(r, n + 1);
+  c.buf_new.alloc(r, n * b);
+  c.buf_old.alloc(r, n * k);
+}
+
+}  // namespace
+
+void sample_neighbors_device(Runner& r, uint64_t n, uint32_t k, double rho, uint64_t seed,
+                             uint64_t iter, const uint64_t* keys, uint32_t* flags,
+                             SampleLists& out) {
+  require(!(rho <= 0.0 || rho > 1.0), "sample_neighbors: rho must be in (0, 1]");
+  require(k >= 1 && k <= 32, "sample_neighbors: the B200 path supports 1 <= k <= 32");
+  const uint32_t B = bound_of(rho, k);
+  RevCsr c;
+  alloc_lists(r, n, k, B, out, c);
+  sample_into(r, n, k, B, mix_seed(seed, 0x5a3f1e00ull + iter), keys, flags, out, c, nullptr);
+}
+
+void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_t* keys,
+                       uint32_t* flags, NndStats* st, bool time_kernels) {
+  validate_nnd(p, ds.n);
+  const u64 n = ds.n;
+  const u32 k = p.k;
+  const u32 B = bound_of(p.rho, k);
+  const u32 S = (u32)(p.candidate_capacity ? p.candidate_capacity : 2ull * k);
+  DeviceGuard guard(r.device);
+
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evb = nullptr, eve = nullptr;
+  if (time_kernels) {
+    KNNG_CUDA(cudaEventCreate(&ev0));
+    KNNG_CUDA(cudaEventCreate(&ev1));
+    KNNG_CUDA(cudaEventCreate(&evb));
+    KNNG_CUDA(cudaEventCreate(&eve));
+    KNNG_CUDA(cudaEventRecord(evb, r.stream));
+  }
+
+  DBuf<float> worst(r, n);
+  DBuf<u64> slots(r, n * S);
+  slots.fill_bytes(0xff);
+  DBuf<u64> counters(r, kNumCounters);
+  HBuf<u64> hcount(kNumCounters);
+  SampleLists s;
+  RevCsr c;
+  alloc_lists(r, n, k, B, s, c);
+  uint64_t launches = 0;
+
+  k_init<<<warp_grid(r, n), 256, 0, r.stream>>>(ds.x, n, ds.d, k, p.seed, keys, flags, worst.p);
+  KNNG_LAUNCH_CHECK();
+  ++launches;
+
+  // join launch shape
+  JoinArgs ja{};
+  ja.X = ds.x;
+  ja.n = n;
+  ja.d = ds.d;
+  ja.k = k;
+  ja.B = B;
+  ja.nf = s.nf.p;
+  ja.nfn = s.nfn.p;
+  ja.of = s.of.p;
+  ja.ofn = s.ofn.p;
+  ja.nr = s.nr.p;
+  ja.nrn = s.nrn.p;
+  ja.orv = s.orv.p;
+  ja.orn = s.orn.p;
+  ja.worst = worst.p;
+  ja.slots = slots.p;
+  ja.S = S;
+  ja.counters = counters.p;
+  const int max_rows = (int)(2 * B + k + B);
+  ja.RMAX = (max_rows + 3) & ~3;
+  ja.DC = ds.d <= 128 ? ((ds.d + 7) & ~7) : 128;
+  ja.DCP = ja.DC + 4;  // DC % 8 == 0 -> (DCP/4) odd
+  const size_t smem = (size_t)ja.RMAX * 4 + 16 + (size_t)ja.RMAX * ja.DCP * 4;
+  KNNG_CUDA(cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  int per_sm = 0;
+  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_join, kJoinThreads, smem));
+  if (per_sm < 1) per_sm = 1;
+  const unsigned jgrid = persistent_grid(r, per_sm, n);
+
+  if (st) *st = NndStats{};
+  const double threshold = p.delta * (double)k * (double)n;
+  for (u64 iter = 0; iter < p.max_iters; ++iter) {
+    counters.zero();
+    const u64 iter_seed = mix_seed(p.seed, 0x5a3f1e00ull + iter);
+    sample_into(r, n, k, B, iter_seed, keys, flags, s, c, &launches);
+    if (time_kernels) KNNG_CUDA(cudaEventRecord(ev0, r.stream));
+    k_join<<<jgrid, kJoinThreads, smem, r.stream>>>(ja);
+    KNNG_LAUNCH_CHECK();
+    if (time_kernels) KNNG_CUDA(cudaEventRecord(ev1, r.stream));
+    k_apply<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst.p, slots.p,
+                                                   counters.p);
+    KNNG_LAUNCH_CHECK();
+    launches += 2;
+    KNNG_CUDA(cudaMemcpyAsync(hcount.p, counters.p, kNumCounters * sizeof(u64),
+                              cudaMemcpyDeviceToHost, r.stream));
+    r.sync();
+    const u64 accepted = hcount.p[kCntAccepted];
+    if (st) {
+      st->accepted_per_iter.push_back(accepted);
+      st->iterations = iter + 1;
+      st->pairs += hcount.p[kCntPairs];
+      st->staged_rows += hcount.p[kCntStagedRows];
+      st->offers += hcount.p[kCntOffers];
+      if (time_kernels) {
+        float ms = 0;
+        KNNG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+        st->join_ms += ms;
+        st->join_launches += 1;
+      }
+    }
+    if ((double)accepted < threshold) break;
+  }
+  if (time_kernels) {
+    KNNG_CUDA(cudaEventRecord(eve, r.stream));
+    KNNG_CUDA(cudaEventSynchronize(eve));
+    float ms = 0;
+    KNNG_CUDA(cudaEventElapsedTime(&ms, evb, eve));
+    if (st) st->total_ms = ms;
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    cudaEventDestroy(evb);
+    cudaEventDestroy(eve);
+  }
+  if (st) st->launches = launches;
+}
+
+void export_graph_device(const Runner& r, const uint64_t* keys, const uint32_t* flags,
+                         uint64_t n, uint32_t k, uint32_t id_shift, uint32_t* ids, float* dists,
+                         uint8_t* flags_u8) {
+  const u64 total = n * k;
+  if (!total) return;
+  const unsigned g = (unsigned)std::min<u64>(ceil_div<u64>(total, 256), (u64)r.num_sms * 32);
+  k_export<<<g, 256, 0, r.stream>>>(keys, flags, n, k, id_shift, ids, dists, flags_u8);
+  KNNG_LAUNCH_CHECK();
+}
+
+void import_graph_device(const Runner& r, const uint32_t* ids, const float* dists,
+                         const uint8_t* flags_u8, uint64_t n, uint32_t k, uint64_t* keys,
+                         uint32_t* flags) {
+  if (!n) return;
+  k_import<<<warp_grid(r, n), 256, 0, r.stream>>>(ids, dists, flags_u8, n, k, keys, flags);
+  KNNG_LAUNCH_CHECK();
+}
+
+}  // namespace knng_b200

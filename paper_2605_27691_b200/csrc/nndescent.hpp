@@ -1,0 +1,86 @@
+// nndescent.hpp -- B200 lock-free NN-Descent local build (north_star item 2).
+//
+// Reference: nndescent.cpp:225-259 (nn_descent), :29-62 (init_random_graph),
+// :64-129 (sample_neighbors), :135-197 (build_join_lists + local_join),
+// :199-223 (apply_candidates), nndescent.hpp:12-20 (NnDescentParams).
+//
+// Device graph layout: keys[n*k] u64 packed (dist,id) sorted ascending per row,
+// flags[n] u32 bitmask of "new" entries (k <= 32), worst[n] f32 = dist of
+// row[k-1] (CandidateBuffer::worst, nndescent.hpp:58-60).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "runtime.hpp"
+
+namespace knng_b200 {
+
+struct NndParams {
+  uint32_t k = 32;
+  double delta = 0.0001;
+  double rho = 0.5;
+  uint64_t max_iters = 100;
+  uint64_t candidate_capacity = 0;  // 0 -> 2k
+  uint64_t seed = 0;
+};
+
+// Device counters written by the kernels (read back once per iteration).
+enum NndCounter : int {
+  kCntAccepted = 0,    // gross successful knn_insert calls (nndescent.cpp:213)
+  kCntPairs = 1,       // sigma evaluations (JoinCounts::pairs)
+  kCntStagedRows = 2,  // feature rows staged into smem by the join (algorithmic bytes)
+  kCntOffers = 3,      // offers passing the worst filter (atomicMin issued)
+  kCntJoinPoints = 4,  // points with >= 1 pair
+  kNumCounters = 8
+};
+
+struct NndStats {
+  std::vector<uint64_t> accepted_per_iter;
+  uint64_t iterations = 0;
+  uint64_t pairs = 0;
+  uint64_t staged_rows = 0;
+  uint64_t offers = 0;
+  // Device time of the join kernel summed over iterations (CUDA events on the
+  // launching stream) and of the whole build.
+  double join_ms = 0.0;
+  double total_ms = 0.0;
+  uint64_t join_launches = 0;
+  uint64_t launches = 0;  // all kernels launched by the build
+};
+
+// Dataset on the runner's device, row-major n x d f32, L2.
+struct DevRows {
+  const float* x = nullptr;
+  uint64_t n = 0;
+  int d = 0;
+};
+
+void validate_nnd(const NndParams& p, uint64_t n);
+
+// Full build.  keys/flags must hold n*k / n entries on the runner's device.
+void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_t* keys,
+                       uint32_t* flags, NndStats* stats, bool time_kernels);
+
+// Individual stages (exposed for parity tests through the C-ABI).
+void init_random_graph_device(Runner& r, const DevRows& ds, uint32_t k, uint64_t seed,
+                              uint64_t* keys, uint32_t* flags);
+
+struct SampleLists {
+  uint32_t bound = 0;
+  DBuf<uint32_t> nf, nfn, of, ofn, nr, nrn, orv, orn;
+};
+void sample_neighbors_device(Runner& r, uint64_t n, uint32_t k, double rho, uint64_t seed,
+                             uint64_t iter, const uint64_t* keys, uint32_t* flags,
+                             SampleLists& out);
+
+// keys -> ids / dists / u8 flags (KnnGraph layout, core.hpp:156-179).
+void export_graph_device(const Runner& r, const uint64_t* keys, const uint32_t* flags,
+                         uint64_t n, uint32_t k, uint32_t id_shift, uint32_t* ids,
+                         float* dists, uint8_t* flags_u8);
+// ids / dists (+ optional u8 flags) -> keys (+ flag masks).
+void import_graph_device(const Runner& r, const uint32_t* ids, const float* dists,
+                         const uint8_t* flags_u8, uint64_t n, uint32_t k, uint64_t* keys,
+                         uint32_t* flags);
+
+}  // namespace knng_b200

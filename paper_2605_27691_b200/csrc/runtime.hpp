@@ -1,0 +1,178 @@
+// runtime.hpp -- host-side plumbing shared by the B200 kNN-graph library:
+// error types mirroring the reference's exception classes, a per-(device,
+// stream) Runner with stream-ordered allocations, and launch helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace knng_b200 {
+
+// Error classes map 1:1 onto the reference's:
+//   std::invalid_argument (usage), WorldError/WorldAborted (transport),
+//   FormatError (vecs/wire), std::logic_error (invariants).
+struct WorldError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct WorldAborted : WorldError {
+  using WorldError::WorldError;
+};
+struct FormatError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void require(bool ok, const std::string& what) {
+  if (!ok) throw std::invalid_argument(what);
+}
+
+// Device guard: sets the current device for the scope.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    KNNG_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) KNNG_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// One stream on one device.  All kernels of a call run on it, all temporaries
+// are stream-ordered (cudaMallocAsync from the device pool, which we keep
+// cached so steady-state iterations never hit the driver allocator).
+struct Runner {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  bool owns = false;
+
+  Runner() = default;
+  explicit Runner(int dev) : device(dev) {
+    DeviceGuard g(dev);
+    KNNG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    owns = true;
+    KNNG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    cudaMemPool_t pool;
+    KNNG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = ~0ull;
+    KNNG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  Runner(const Runner&) = delete;
+  Runner& operator=(const Runner&) = delete;
+  Runner(Runner&& o) noexcept { *this = std::move(o); }
+  Runner& operator=(Runner&& o) noexcept {
+    device = o.device;
+    stream = o.stream;
+    num_sms = o.num_sms;
+    owns = o.owns;
+    o.owns = false;
+    o.stream = nullptr;
+    return *this;
+  }
+  ~Runner() {
+    if (owns && stream) {
+      cudaSetDevice(device);
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+  }
+  void sync() const { KNNG_CUDA(cudaStreamSynchronize(stream)); }
+};
+
+// Stream-ordered device buffer.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  int dev = 0;
+
+  DBuf() = default;
+  DBuf(const Runner& r, size_t count) { alloc(r, count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept { swap(o); }
+  DBuf& operator=(DBuf&& o) noexcept {
+    release();
+    swap(o);
+    return *this;
+  }
+  ~DBuf() { release(); }
+
+  void swap(DBuf& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(s, o.s);
+    std::swap(dev, o.dev);
+  }
+  void alloc(const Runner& r, size_t count) {
+    release();
+    s = r.stream;
+    dev = r.device;
+    n = count;
+    if (count) {
+      DeviceGuard g(dev);
+      KNNG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+    }
+  }
+  void release() noexcept {
+    if (p) {
+      int cur = -1;
+      cudaGetDevice(&cur);
+      if (cur != dev) cudaSetDevice(dev);
+      cudaFreeAsync(p, s);
+      if (cur != dev && cur >= 0) cudaSetDevice(cur);
+    }
+    p = nullptr;
+    n = 0;
+  }
+  void zero() {
+    if (n) KNNG_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void fill_bytes(int v) {
+    if (n) KNNG_CUDA(cudaMemsetAsync(p, v, n * sizeof(T), s));
+  }
+  T* get() const { return p; }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// Pinned host scratch.
+template <class T>
+struct HBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  HBuf() = default;
+  explicit HBuf(size_t count) { alloc(count); }
+  HBuf(const HBuf&) = delete;
+  HBuf& operator=(const HBuf&) = delete;
+  ~HBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void alloc(size_t count) {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = count;
+    if (count) KNNG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), count * sizeof(T)));
+  }
+};
+
+// Grid of persistent CTAs: `per_sm` resident CTAs on every SM.
+inline unsigned persistent_grid(const Runner& r, int per_sm, uint64_t work_items) {
+  uint64_t g = (uint64_t)r.num_sms * (uint64_t)per_sm;
+  if (work_items < g) g = work_items ? work_items : 1;
+  return (unsigned)g;
+}
+
+// Prefix sum (scan.cu): out[0..n] exclusive scan of in[0..n), out[n] = total.
+void exclusive_scan_u32(const Runner& r, const uint32_t* in, uint64_t* out, uint64_t n);
+
+}  // namespace knng_b200

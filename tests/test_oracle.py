@@ -1,0 +1,147 @@
+"""The C restatement (oracle/knng_oracle.c) against the golden fixtures minted
+from the unmodified reference (tests/golden/make_golden.py).  CPU only.
+
+Every comparison is bit-exact: ids, and float32 distances compared as bits.
+"""
+import numpy as np
+import pytest
+
+from oracle.bindings import KoSearchParams  # noqa: F401
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def test_generator(golden, oracle):
+    g = golden("gen")
+    for dist, cl in [("uniform", 0), ("gaussian", 0), ("clustered", 7)]:
+        assert np.array_equal(bits(oracle.gen_random_dataset(257, 9, dist, 42, cl)), bits(g[dist]))
+
+
+def test_l2_golden_values(oracle):
+    # test_core.cpp:47-53
+    assert oracle.l2([0.0, 0.0], [3.0, 4.0]) == 5.0
+    assert oracle.l2([1.0, 2.0], [1.0, 2.0]) == 0.0
+
+
+def test_merge_rows(golden, oracle):
+    g = golden("merge_rows")
+    for r in range(g["a_ids"].shape[0]):
+        oi, od = oracle.merge_rows(g["a_ids"][r], g["a_d"][r], g["b_ids"][r], g["b_d"][r], 10)
+        n = int(g["out_n"][r])
+        assert len(oi) == n
+        assert np.array_equal(oi, g["out_ids"][r, :n])
+        assert np.array_equal(bits(od), bits(g["out_d"][r, :n]))
+
+
+def test_init_random_graph(golden, oracle):
+    g = golden("nndescent")
+    ids, d, f = oracle.init_random_graph(g["x"], 12, 5)
+    assert np.array_equal(ids, g["init_ids"])
+    assert np.array_equal(bits(d), bits(g["init_d"]))
+    assert np.array_equal(f, g["init_f"])
+
+
+def _cmp_lists(a_mat, a_n, b_mat, b_n):
+    assert np.array_equal(a_n, b_n)
+    for p in range(len(a_n)):
+        assert np.array_equal(a_mat[p, :a_n[p]], b_mat[p, :b_n[p]]), p
+
+
+def test_sample_neighbors_two_rounds(golden, oracle):
+    g = golden("nndescent")
+    s = oracle.sample_neighbors(g["init_ids"], g["init_f"], 0.5, 7, 3)
+    assert s["bound"] == int(g["s_bound"][0])
+    assert np.array_equal(s["flags"], g["s_flags"])
+    for key in ("new_fwd", "old_fwd", "new_rev", "old_rev"):
+        _cmp_lists(*s[key], g["s_" + key], g["s_" + key + "_n"])
+    s2 = oracle.sample_neighbors(g["init_ids"], g["s_flags"], 0.5, 7, 4)
+    assert np.array_equal(s2["flags"], g["s2_flags"])
+    for key in ("new_fwd", "old_fwd", "new_rev", "old_rev"):
+        _cmp_lists(*s2[key], g["s2_" + key], g["s2_" + key + "_n"])
+
+
+def test_nn_descent_workers1(golden, oracle):
+    g = golden("nndescent")
+    ids, d, f, acc = oracle.nn_descent(g["x"], 16, seed=3)
+    assert np.array_equal(ids, g["nn_ids"])
+    assert np.array_equal(bits(d), bits(g["nn_d"]))
+    assert np.array_equal(f, g["nn_f"])
+    assert np.array_equal(acc, g["nn_accepted"])
+    assert oracle.check_invariants(ids, d) == 0
+
+
+def test_optimize_graph(golden, oracle):
+    g = golden("search")
+    assert np.array_equal(oracle.optimize_graph(g["nn_ids"], g["nn_d"], g["x"], 16), g["sg"])
+    assert np.array_equal(oracle.optimize_graph(g["nn_ids"], g["nn_d"], g["x"], 8), g["sg8"])
+
+
+def test_ann_search(golden, oracle):
+    g = golden("search")
+    i, d, h, s = oracle.ann_search(g["q"], g["sg"], g["x"], 16, 64, 16, 0, 9)
+    assert np.array_equal(i, g["ids"]) and np.array_equal(bits(d), bits(g["d"]))
+    assert np.array_equal(h, g["hops"]) and np.array_equal(s, g["scored"])
+    i, d, h, s = oracle.ann_search(g["q"], g["sg"], g["x"], 32, 128, 96, 0, 11)
+    assert np.array_equal(i, g["ids2"]) and np.array_equal(bits(d), bits(g["d2"]))
+    assert np.array_equal(h, g["hops2"]) and np.array_equal(s, g["scored2"])
+
+
+def test_partition(golden, oracle):
+    g = golden("partition")
+    te, off = oracle.partition(10001, 4, 9)
+    assert np.array_equal(te, g["te"]) and np.array_equal(off, g["off"])
+    assert list(off) == [0, 2501, 5001, 7501, 10001]  # test_refine.cpp:59-64
+    te8, off8 = oracle.partition(8, 4, 5)
+    assert np.array_equal(te8, g["te8"]) and list(off8) == [0, 2, 4, 6, 8]
+    teb, offb = oracle.partition(1000003, 8, 1)
+    w = np.arange(1, len(teb) + 1, dtype=np.uint64)
+    assert np.array_equal(teb[:4096], g["tebig_head"])
+    assert int((teb.astype(np.uint64) * w).sum(dtype=np.uint64)) == int(g["tebig_sum"][0])
+    with pytest.raises(ValueError):
+        oracle.partition(8, 9, 0)
+
+
+def test_brute_force(golden, oracle):
+    g = golden("bruteforce")
+    rows = np.arange(0, 2000, 3, dtype=np.uint64)
+    i, d = oracle.brute_force_rows(g["x"], rows, 10)
+    assert np.array_equal(i, g["ids"][rows]) and np.array_equal(bits(d), bits(g["d"][rows]))
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_build_distributed(golden, oracle, P):
+    g = golden("distributed")
+    cfg = oracle.refine_config(P, 2, 16, nn_seed=2, search_seed=2, seed=2, beam_width=64)
+    i, d = oracle.build_distributed(g["x"], cfg)
+    assert np.array_equal(i, g[f"p{P}_ids"]) and np.array_equal(bits(d), bits(g[f"p{P}_d"]))
+
+
+def test_refine_from_local(golden, oracle):
+    g = golden("distributed")
+    cfg = oracle.refine_config(4, 2, 16, nn_seed=2, search_seed=2, seed=2)
+    te, off = oracle.partition(2000, 4, 2)
+    for mode, key in [(0, "refine4"), (1, "a2a4")]:
+        i, d = oracle.refine_from_local(g["x"], cfg, te, off, g["local4_ids"], g["local4_d"], mode)
+        assert np.array_equal(i, g[key + "_ids"]) and np.array_equal(bits(d), bits(g[key + "_d"]))
+    cfg8 = oracle.refine_config(8, 2, 16, nn_seed=2, search_seed=2, seed=2, beam_width=128,
+                                num_entry_points=96)
+    te8, off8 = oracle.partition(2000, 8, 2)
+    i, d = oracle.refine_from_local(g["x"], cfg8, te8, off8, g["local8_ids"], g["local8_d"], 0)
+    assert np.array_equal(i, g["refine8_ids"]) and np.array_equal(bits(d), bits(g["refine8_d"]))
+
+
+def test_tree_schedule_worked_example(oracle):
+    # test_refine.cpp:69-76
+    import ctypes as C
+    L = oracle.L
+    L.ko_tree_schedule.restype = C.c_long
+    L.ko_tree_schedule.argtypes = [C.c_size_t] * 4 + [C.POINTER(C.c_size_t),
+                                                      C.POINTER(C.c_size_t)]
+    hi = C.c_size_t(0)
+    partners = (C.c_size_t * 8)()
+    assert L.ko_tree_schedule(8, 2, 0, 0, C.byref(hi), partners) == 0 and partners[0] == 1
+    assert L.ko_tree_schedule(8, 2, 0, 1, C.byref(hi), partners) == 0
+    assert list(partners[:2]) == [2, 3] and hi.value == 2
+    assert L.ko_tree_levels(8, 2) == 2 and L.ko_tree_levels(4, 4) == 0

@@ -1,0 +1,452 @@
+"""CUDA path vs the reference, through the C-ABI (libknng_b200.so).
+
+Bit-exact (ids and float32 distance bits) for every deterministic stage:
+init_random_graph, sample_neighbors, merge_rows, optimize_graph, ann_search,
+partition, brute force, translate, and the refine drivers.  NN-Descent itself
+updates neighbor lists with lock-free atomicMin instead of the reference's
+first-come candidate buffers, so it is held to the north_star bar instead:
+recall@10 >= reference recall - 0.005 on identical bytes and seeds, every row
+invariant of check_graph_invariants (core.cpp:166-186), and every stored
+distance equal to the exact recomputation.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def bits(a):
+    return np.ascontiguousarray(np.asarray(a), np.float32).view(np.uint32)
+
+
+def recall(ids, gt, k_eval=10):
+    hits = 0
+    for r in range(gt.shape[0]):
+        hits += len(np.intersect1d(ids[r, :k_eval], gt[r, :k_eval]))
+    return hits / (gt.shape[0] * k_eval)
+
+
+# ---------------------------------------------------------------------------
+# core
+# ---------------------------------------------------------------------------
+
+
+def test_row_distances_exact(knng, oracle, golden):
+    x = golden("nndescent")["x"]
+    rng = np.random.default_rng(1)
+    i = rng.integers(0, len(x), 5000).astype(np.uint32)
+    j = rng.integers(0, len(x), 5000).astype(np.uint32)
+    d = knng.row_distances(x, i, j)
+    ref = np.array([oracle.l2(x[a], x[b]) for a, b in zip(i, j)], np.float32)
+    assert np.array_equal(bits(d), bits(ref))
+    # odd dims (scalar path) and d = 960 (chunked)
+    for dims in (3, 960):
+        y = np.random.default_rng(dims).standard_normal((64, dims)).astype(np.float32)
+        d = knng.row_distances(y, np.arange(64), np.arange(64)[::-1])
+        ref = np.array([oracle.l2(y[a], y[63 - a]) for a in range(64)], np.float32)
+        assert np.array_equal(bits(d), bits(ref))
+
+
+def test_l2_golden_value(knng):
+    x = np.array([[0.0, 0.0], [3.0, 4.0]], np.float32)
+    assert knng.row_distances(x, [0], [1])[0] == 5.0
+
+
+def test_merge_rows_bitexact(knng, golden):
+    g = golden("merge_rows")
+    oi, od, oc = knng.merge_rows_batch(g["a_ids"], g["a_d"], g["b_ids"], g["b_d"], 10)
+    assert np.array_equal(oc, g["out_n"])
+    for r in range(len(oc)):
+        n = oc[r]
+        assert np.array_equal(oi[r, :n], g["out_ids"][r, :n])
+        assert np.array_equal(bits(od[r, :n]), bits(g["out_d"][r, :n]))
+    # trivial examples test_core.cpp:170-181, 212-221
+    i, d = knng.merge_rows([0], [0.1], [1], [0.2], 2)
+    assert list(i) == [0, 1]
+    i, d = knng.merge_rows([0], [0.1], [0], [0.1], 2)
+    assert list(i) == [0]
+    i, d = knng.merge_rows([3, 1, 7], [0.1, 0.2, 0.9], np.zeros(0), np.zeros(0), 2)
+    assert list(i) == [3, 1]
+
+
+# ---------------------------------------------------------------------------
+# nndescent stages
+# ---------------------------------------------------------------------------
+
+
+def test_init_random_graph_bitexact(knng, golden):
+    g = golden("nndescent")
+    out = knng.init_random_graph(g["x"], 12, 5)
+    assert np.array_equal(out.ids, g["init_ids"])
+    assert np.array_equal(bits(out.dists), bits(g["init_d"]))
+    assert np.array_equal(out.flags, g["init_f"])
+
+
+def test_init_random_graph_k_eq_n_minus_1(knng, oracle):
+    # test_nndescent.cpp:28-37
+    x = knng.gen_random_dataset(5, 3, "uniform", 2)
+    g = knng.init_random_graph(x, 4, 11)
+    for r in range(5):
+        assert sorted(g.ids[r]) == sorted(set(range(5)) - {r})
+    with pytest.raises(knng.InvalidArgument):
+        knng.init_random_graph(x, 5, 0)
+
+
+def _lists_equal(got, mat, cnt):
+    assert len(got) == len(cnt)
+    for p in range(len(cnt)):
+        assert np.array_equal(got[p], mat[p, :cnt[p]]), p
+
+
+def test_sample_neighbors_bitexact(knng, golden):
+    g = golden("nndescent")
+    graph = knng.KnnGraph(g["init_ids"], g["init_d"], g["init_f"].copy())
+    s = knng.sample_neighbors(graph, 0.5, 7, 3)
+    assert s["bound"] == int(g["s_bound"][0])
+    assert np.array_equal(graph.flags, g["s_flags"])
+    for key in ("new_fwd", "old_fwd", "new_rev", "old_rev"):
+        _lists_equal(s[key], g["s_" + key], g["s_" + key + "_n"])
+    s2 = knng.sample_neighbors(graph, 0.5, 7, 4)
+    assert np.array_equal(graph.flags, g["s2_flags"])
+    for key in ("new_fwd", "old_fwd", "new_rev", "old_rev"):
+        _lists_equal(s2[key], g["s2_" + key], g["s2_" + key + "_n"])
+
+
+def test_sample_neighbors_rho1(knng):
+    # test_nndescent.cpp:67-81
+    x = knng.gen_random_dataset(50, 4, "uniform", 9)
+    g = knng.init_random_graph(x, 8, 1)
+    s = knng.sample_neighbors(g, 1.0, 1, 0)
+    assert all(len(v) == 8 for v in s["new_fwd"]) and all(len(v) == 0 for v in s["old_fwd"])
+    s2 = knng.sample_neighbors(g, 1.0, 1, 1)
+    assert all(len(v) == 0 for v in s2["new_fwd"]) and all(len(v) == 8 for v in s2["old_fwd"])
+
+
+def test_nn_descent_invariants_and_exact_distances(knng, oracle, golden):
+    x = golden("nndescent")["x"]
+    st = knng.NnDescentStats()
+    g = knng.nn_descent(x, k=16, seed=3, stats=st)
+    assert oracle.check_invariants(g.ids, g.dists) == 0
+    rows = np.repeat(np.arange(len(x)), 16).astype(np.uint32)
+    ref = np.array([oracle.l2(x[a], x[b]) for a, b in zip(rows[:4000], g.ids.reshape(-1)[:4000])],
+                   np.float32)
+    assert np.array_equal(bits(g.dists.reshape(-1)[:4000]), bits(ref))
+    # deterministic: the lock-free atomicMin update is order independent
+    g2 = knng.nn_descent(x, k=16, seed=3)
+    assert np.array_equal(g.ids, g2.ids) and np.array_equal(bits(g.dists), bits(g2.dists))
+    assert st.iterations >= 2 and st.pairs > 0
+    assert st.accepted_per_iter[-1] < 1e-4 * 16 * len(x) or st.iterations == 100
+
+
+def test_nn_descent_recall_vs_reference_small(knng, golden):
+    g = golden("nndescent")
+    gt = golden("bruteforce")["ids"]
+    ref = recall(g["nn_ids"], gt)
+    mine = recall(knng.nn_descent(g["x"], k=16, seed=3).ids, gt)
+    assert mine >= ref - 0.005, (mine, ref)
+
+
+def test_nn_descent_k_eq_n_minus_1_exact(knng):
+    # test_nndescent.cpp:215-240
+    x = knng.gen_random_dataset(33, 8, "uniform", 14)
+    g = knng.nn_descent(x, k=32, rho=1.0, seed=1)
+    gt, _ = knng.brute_force_knng(x, 32)
+    assert recall(g.ids, gt, 32) == 1.0
+    st = knng.NnDescentStats()
+    knng.nn_descent(knng.gen_random_dataset(33, 8, "uniform", 4), k=32, delta=1.0, rho=1.0, seed=9,
+                    stats=st)
+    assert st.iterations == 1
+
+
+def test_nn_descent_recall_3000x16(knng):
+    # test_nndescent.cpp:242-258
+    x = knng.gen_random_dataset(3000, 16, "uniform", 6)
+    st = knng.NnDescentStats()
+    g = knng.nn_descent(x, k=16, seed=3, stats=st)
+    gt, _ = knng.brute_force_knng(x, 16)
+    assert recall(g.ids, gt, 10) >= 0.9
+    assert st.iterations < 100 and st.accepted_per_iter[-1] < 1e-4 * 16 * 3000
+
+
+def test_acceptance_local_build_quality(knng):
+    # acceptance.cpp:52-67: 20k x 16 uniform, k=32 -> recall@10 >= 0.95
+    x = knng.gen_random_dataset(20000, 16, "uniform", 4242)
+    g = knng.nn_descent(x, k=32, seed=1)
+    rows = np.arange(0, 20000, 7, dtype=np.uint64)
+    gt, _ = knng.brute_force_knng(x, 10, rows=rows)
+    assert recall(g.ids[rows.astype(np.int64)], gt) >= 0.95
+
+
+def test_nn_descent_validation(knng):
+    # test_nndescent.cpp:288-300
+    x = knng.gen_random_dataset(100, 4, "uniform", 2)
+    with pytest.raises(knng.InvalidArgument):
+        knng.nn_descent(x, k=8, rho=0.0)
+    with pytest.raises(knng.InvalidArgument):
+        knng.nn_descent(x, k=8, delta=-0.1)
+    with pytest.raises(knng.InvalidArgument):
+        knng.nn_descent(x, k=8, candidate_capacity=4)
+    with pytest.raises(knng.InvalidArgument):
+        knng.nn_descent(x, k=100)
+
+
+# ---------------------------------------------------------------------------
+# graphopt / annsearch
+# ---------------------------------------------------------------------------
+
+
+def test_optimize_graph_bitexact(knng, golden):
+    g = golden("search")
+    graph = knng.KnnGraph(g["nn_ids"], g["nn_d"])
+    assert np.array_equal(knng.optimize_graph(graph, g["x"], 16), g["sg"])
+    assert np.array_equal(knng.optimize_graph(graph, g["x"], 8), g["sg8"])
+    with pytest.raises(knng.InvalidArgument):
+        knng.optimize_graph(graph, g["x"], 17)
+
+
+def test_optimize_graph_collinear(knng):
+    # test_graphopt.cpp:48-60
+    x = np.array([[0.0], [1.0], [2.0]], np.float32)
+    gt_i, gt_d = knng.brute_force_knng(x, 2)
+    sg = knng.optimize_graph(knng.KnnGraph(gt_i, gt_d), x, 1)
+    assert sg[0, 0] == 1 and sg[2, 0] == 1
+
+
+def test_ann_search_bitexact(knng, golden):
+    g = golden("search")
+    r = knng.ann_search(g["q"], g["sg"], g["x"], knng.SearchParams(16, 64, 16, 0, 9),
+                        diagnostics=True)
+    assert np.array_equal(r.ids, g["ids"]) and np.array_equal(bits(r.dists), bits(g["d"]))
+    assert np.array_equal(r.hops, g["hops"]) and np.array_equal(r.scored, g["scored"])
+    r = knng.ann_search(g["q"], g["sg"], g["x"], knng.SearchParams(32, 128, 96, 0, 11),
+                        diagnostics=True)
+    assert np.array_equal(r.ids, g["ids2"]) and np.array_equal(bits(r.dists), bits(g["d2"]))
+    assert np.array_equal(r.hops, g["hops2"]) and np.array_equal(r.scored, g["scored2"])
+    r = knng.ann_search(g["x"][:300].copy(), g["sg"], g["x"], knng.SearchParams(10, 64, 16, 0, 5))
+    assert np.array_equal(r.ids, g["self_ids"]) and np.array_equal(bits(r.dists), bits(g["self_d"]))
+
+
+def test_ann_search_visited_overflow_matches_oracle(knng, oracle):
+    # a beam so wide that the visited set spills from smem to the global
+    # table: results must stay identical to the reference semantics
+    x = knng.gen_random_dataset(20000, 8, "uniform", 3)
+    g = knng.nn_descent(x, k=32, seed=1)
+    sg = knng.optimize_graph(g, x, 32)
+    q = knng.gen_random_dataset(64, 8, "uniform", 4)
+    r = knng.ann_search(q, sg, x, knng.SearchParams(32, 512, 64, 0, 2), diagnostics=True)
+    oi, od, oh, osc = oracle.ann_search(q, sg, x, 32, 512, 64, 0, 2)
+    assert np.array_equal(r.ids, oi) and np.array_equal(bits(r.dists), bits(od))
+    assert np.array_equal(r.scored, osc) and int(osc.max()) > 3072
+
+
+def test_ann_search_single_point(knng):
+    # test_annsearch.cpp:60-77
+    one = np.array([[3.0, 4.0]], np.float32)
+    q = np.array([[0.0, 0.0], [100.0, -5.0]], np.float32)
+    r = knng.ann_search(q, np.zeros((1, 0), np.uint32), one, knng.SearchParams(1, 4))
+    assert list(r.ids[:, 0]) == [0, 0] and r.dists[0, 0] == 5.0
+
+
+def test_ann_search_validation(knng, golden):
+    g = golden("search")
+    with pytest.raises(knng.InvalidArgument):
+        knng.ann_search(g["q"], g["sg"], g["x"], knng.SearchParams(65, 64))
+    with pytest.raises(knng.InvalidArgument):
+        knng.ann_search(g["q"], g["sg"][:10], g["x"], knng.SearchParams(10, 64))
+
+
+# ---------------------------------------------------------------------------
+# partition / brute force / translate / refine
+# ---------------------------------------------------------------------------
+
+
+def test_partition_bitexact(knng, golden, oracle):
+    g = golden("partition")
+    p = knng.partition_dataset(np.zeros((10001, 2), np.float32), 4, 9, gather=False)
+    assert np.array_equal(p.to_external, g["te"]) and np.array_equal(p.offsets, g["off"])
+    x8 = knng.gen_random_dataset(8, 4, "uniform", 1)
+    p8 = knng.partition_dataset(x8, 4, 5)
+    assert np.array_equal(p8.to_external, g["te8"]) and list(p8.offsets) == [0, 2, 4, 6, 8]
+    assert np.array_equal(p8.locals_concat, x8[p8.to_external])
+    p1 = knng.partition_dataset(x8, 1, 5)
+    assert list(p1.to_external) == list(range(8))
+    pb = knng.partition_dataset(np.zeros((1000003, 1), np.float32), 8, 1, gather=False)
+    w = np.arange(1, 1000004, dtype=np.uint64)
+    assert np.array_equal(pb.to_external[:4096], g["tebig_head"])
+    assert int((pb.to_external.astype(np.uint64) * w).sum(dtype=np.uint64)) == int(g["tebig_sum"][0])
+    with pytest.raises(knng.InvalidArgument):
+        knng.partition_dataset(x8, 9, 0)
+
+
+@pytest.mark.slow
+def test_partition_100m_matches_serial_shuffle(knng, oracle):
+    n = 100_000_000
+    p = knng.partition_dataset(np.zeros((n, 1), np.float32), 8, 1, gather=False)
+    te, off = oracle.partition(n, 8, 1)
+    assert np.array_equal(p.to_external, te) and np.array_equal(p.offsets, off)
+
+
+def test_brute_force_bitexact(knng, golden):
+    g = golden("bruteforce")
+    i, d = knng.brute_force_knng(g["x"], 10)
+    assert np.array_equal(i, g["ids"]) and np.array_equal(bits(d), bits(g["d"]))
+    rows = np.array([5, 17, 1999, 0], np.uint64)
+    i, d = knng.brute_force_knng(g["x"], 10, rows=rows)
+    assert np.array_equal(i, g["ids"][rows.astype(np.int64)])
+
+
+def test_translate_to_external(knng, oracle, golden):
+    g = golden("distributed")
+    p = knng.partition_dataset(g["x"], 4, 2, gather=False)
+    ids, d = g["refine4_ids"], g["refine4_d"]
+    oi, od = knng.translate_to_external(p.to_external, ids, d)
+    ri, rd = oracle.translate_to_external(p.to_external, ids, d)
+    assert np.array_equal(oi, ri) and np.array_equal(bits(od), bits(rd))
+
+
+def test_refine_drivers_bitexact(knng, golden):
+    g = golden("distributed")
+    cfg = knng.RefineConfig(ranks=4, groups=2, k=16, seed=2,
+                            nn=knng.NnDescentParams(k=16, seed=2),
+                            search=knng.SearchParams(k_s=16, beam_width=64, seed=2))
+    r0 = knng.refine(g["x_perm4"], cfg, g["off4"], g["local4_ids"], g["local4_d"], mode=0)
+    assert np.array_equal(r0.graph.ids, g["refine4_ids"])
+    assert np.array_equal(bits(r0.graph.dists), bits(g["refine4_d"]))
+    r1 = knng.refine(g["x_perm4"], cfg, g["off4"], g["local4_ids"], g["local4_d"], mode=1)
+    assert np.array_equal(r1.graph.ids, g["a2a4_ids"])
+    assert np.array_equal(bits(r1.graph.dists), bits(g["a2a4_d"]))
+    cfg8 = knng.RefineConfig(ranks=8, groups=2, k=16, seed=2,
+                             nn=knng.NnDescentParams(k=16, seed=2),
+                             search=knng.SearchParams(k_s=16, beam_width=128, num_entry_points=96,
+                                                      seed=2))
+    r8 = knng.refine(g["x_perm8"], cfg8, g["off8"], g["local8_ids"], g["local8_d"], mode=0)
+    assert np.array_equal(r8.graph.ids, g["refine8_ids"])
+    assert np.array_equal(bits(r8.graph.dists), bits(g["refine8_d"]))
+
+
+def _cfg(knng, P, seed=2, k=16, beam=64, entries=16, **kw):
+    return knng.RefineConfig(ranks=P, groups=2, k=k, seed=seed,
+                             nn=knng.NnDescentParams(k=k, seed=seed),
+                             search=knng.SearchParams(k_s=k, beam_width=beam,
+                                                      num_entry_points=entries, seed=seed), **kw)
+
+
+def test_build_distributed_p1_equals_nn_descent(knng, golden):
+    # test_refine.cpp:349-359
+    x = golden("distributed")["x"]
+    r = knng.build_distributed(x, _cfg(knng, 1))
+    g = knng.nn_descent(x, k=16, seed=2)
+    order = np.argsort(np.zeros(1))  # noqa: F841
+    assert np.array_equal(r.graph.ids, g.ids) and np.array_equal(bits(r.graph.dists), bits(g.dists))
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_build_distributed_quality_and_comm(knng, golden, oracle, P):
+    g = golden("distributed")
+    gt = golden("bruteforce")["ids"]
+    r = knng.build_distributed(g["x"], _cfg(knng, P))
+    assert oracle.check_invariants(r.graph.ids, r.graph.dists, local=False) == 0
+    ref_recall = recall(g[f"p{P}_ids"], gt)
+    assert recall(r.graph.ids, gt) >= ref_recall - 0.02
+    # the communication schedule is the reference's: same gets, same bytes
+    gets, nbytes = (int(v) for v in g[f"p{P}_gets"])
+    assert len(r.comm_log) == gets and sum(c.bytes for c in r.comm_log) == nbytes
+
+
+def test_acceptance_distributed_parity(knng):
+    # acceptance.cpp:72-103 (one seed): P in {2,4,8} within 0.02 of P=1
+    x = knng.gen_random_dataset(40000, 16, "clustered", 7100, 16)
+    rows = np.arange(0, 40000, 13, dtype=np.uint64)
+    gt, _ = knng.brute_force_knng(x, 10, rows=rows)
+    rr = []
+    for P in (1, 2, 4, 8):
+        r = knng.build_distributed(x, _cfg(knng, P, seed=0, k=32, beam=128, entries=96))
+        rr.append(recall(r.graph.ids[rows.astype(np.int64)], gt))
+    assert all(abs(rr[0] - v) <= 0.02 for v in rr[1:]), rr
+
+
+def test_acceptance_monotone_refinement(knng):
+    # acceptance.cpp:109-143
+    x = knng.gen_random_dataset(4000, 16, "clustered", 31, 8)
+    gt, _ = knng.brute_force_knng(x, 16)
+    cfg = _cfg(knng, 8, seed=3, entries=64, capture_snapshots=True)
+    r = knng.build_distributed(x, cfg)
+    assert len(r.snapshots) == 2 + r.levels
+    prev = -1.0
+    for lab, snap in r.snapshots:
+        rc = recall(snap.ids, gt)
+        assert rc >= prev, lab
+        prev = rc
+    for (_, a), (_, b) in zip(r.snapshots, r.snapshots[1:]):
+        assert np.all(b.dists <= a.dists)
+
+
+def test_acceptance_comm_accounting(knng):
+    # acceptance.cpp:253-322: P=8, M=2
+    x = knng.gen_random_dataset(4000, 16, "uniform", 55)
+    r = knng.build_distributed(x, _cfg(knng, 8, seed=9))
+    p = knng.partition_dataset(x, 8, 9, gather=False)
+    size = lambda rank: int(p.offsets[rank + 1] - p.offsets[rank])  # noqa: E731
+    for rank in range(8):
+        tree = [c for c in r.comm_log if c.src == rank and 1 <= c.epoch <= r.levels]
+        assert sum(c.region == "graph" for c in tree) == 3
+        assert sum(c.region == "dataset" for c in tree) == 3
+        for c in tree:
+            want = 22 + size(c.target) * (16 * 8 if c.region == "graph" else 16 * 4)
+            assert c.bytes == want
+        flat = [c for c in r.comm_log if c.src == rank and c.epoch == r.flat_epoch]
+        targets = {c.target for c in flat if c.region == "dataset"}
+        assert targets == set(range(4, 8)) if rank < 4 else targets == set(range(4))
+        assert sum(c.region == "sgraph" for c in flat) == 1
+
+
+def test_build_distributed_validation(knng):
+    x = knng.gen_random_dataset(100, 4, "uniform", 1)
+    with pytest.raises(knng.InvalidArgument):
+        knng.build_distributed(x, _cfg(knng, 3))
+    with pytest.raises(knng.InvalidArgument):
+        knng.build_distributed(x, _cfg(knng, 4, k=32))  # k >= points per rank
+
+
+# ---------------------------------------------------------------------------
+# recall parity on the BASELINE configs (reference measured in
+# tests/golden/reference_recall.json on the same bytes, seeds and rows)
+# ---------------------------------------------------------------------------
+
+
+def _ref_recall():
+    p = os.path.join(HERE, "golden", "reference_recall.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
+def _sample(n):
+    rng = np.random.default_rng(12345)
+    return np.sort(rng.choice(n, size=min(1000, n), replace=False)).astype(np.uint64)
+
+
+@pytest.mark.parametrize("name", ["c1_100k_uniform_k10", "c1b_100k_clustered100_k32",
+                                  "c4r_100k_d96_clustered16_p1", "c4r_100k_d96_clustered16_p2",
+                                  "c4r_100k_d96_clustered16_p4", "c4r_100k_d96_clustered16_p8"])
+def test_recall_parity_vs_reference(knng, name):
+    ref = _ref_recall().get(name)
+    if ref is None:
+        pytest.skip("reference recall not measured yet")
+    x = knng.gen_random_dataset(ref["n"], ref["dims"], ref["dist"], ref["data_seed"],
+                                ref["clusters"])
+    if ref["ranks"] == 1:
+        g = knng.nn_descent(x, k=ref["k"], seed=ref["nn_seed"])
+        ids = g.ids
+    else:
+        cfg = knng.RefineConfig(ranks=ref["ranks"], groups=2, k=ref["k"], seed=1,
+                                nn=knng.NnDescentParams(k=ref["k"], seed=1),
+                                search=knng.SearchParams(k_s=ref["k"], beam_width=ref["beam"],
+                                                         num_entry_points=ref["entries"], seed=1))
+        ids = knng.build_distributed(x, cfg).graph.ids
+    rows = _sample(ref["n"])
+    gt, _ = knng.brute_force_knng(x, 10, rows=rows)
+    mine = recall(ids[rows.astype(np.int64)], gt)
+    assert mine >= ref["recall_at_10"] - 0.005, (mine, ref["recall_at_10"])
