@@ -10,9 +10,10 @@
 //   k_join         CTA per point: dedup'd new/old lists (:135-153), feature
 //                  rows staged in smem with cp.async (16 B), 4x4 register
 //                  micro-tiles of exact-order distances, offers (:157-197)
-//                  resolved by 64-bit packed (dist,id) atomicMin into hashed
-//                  candidate slots -- lock-free, order-independent, so the
-//                  build is deterministic regardless of scheduling.
+//                  resolved by 64-bit packed (dist,id) atomicMin cascades
+//                  into hashed 4-way candidate buckets that keep the 4
+//                  smallest distinct keys -- lock-free and order-independent,
+//                  so the build is deterministic regardless of scheduling.
 //   k_apply        warp per point: knn_insert of every surviving slot in slot
 //                  order (:199-223), gross accepted count, worst refresh.
 #include <cmath>
@@ -23,18 +24,38 @@ namespace knng_b200 {
 namespace {
 
 constexpr u32 kNone = 0xffffffffu;
+constexpr u32 kWays = 4;  // candidate slots per hash bucket
 
 __device__ __forceinline__ u32 kmask_of(u32 k) { return k >= 32 ? kFull : ((1u << k) - 1u); }
 
-// Slot of candidate v in point u's hashed candidate buffer.
-__device__ __forceinline__ u32 slot_hash(u32 u, u32 v, u32 S) {
+// Bucket of candidate v in point u's candidate buffer (kWays slots each).
+__device__ __forceinline__ u32 bucket_hash(u32 u, u32 v, u32 nb) {
   u32 x = v * 0x9E3779B1u + u * 0x85EBCA77u;
   x ^= x >> 15;
   x *= 0x2C1B3C6Du;
   x ^= x >> 12;
   x *= 0x297A2D39u;
   x ^= x >> 15;
-  return x % S;
+  return x % nb;
+}
+
+// Lock-free offer: the bucket keeps its kWays smallest distinct (dist,id)
+// keys in ascending order.  Each step atomicMin's the carried key into one
+// slot and carries the larger of (old, key) onward; slots only decrease, so
+// whatever the interleaving the final bucket is the W smallest distinct keys
+// offered -- the update is order-independent and the build deterministic.
+// A key that already cannot beat the bucket's last slot is dropped without
+// an atomic (it could never be among the W smallest).
+__device__ __forceinline__ void offer(u64* __restrict__ bucket, u32 ways, u64 key) {
+  const u64 tail = *reinterpret_cast<volatile u64*>(bucket + ways - 1);
+  if (key >= tail) return;
+  for (u32 w = 0; w < ways; ++w) {
+    const u64 old = atomicMin(reinterpret_cast<unsigned long long*>(bucket + w),
+                              (unsigned long long)key);
+    if (old == key) return;       // duplicate of a buffered candidate
+    key = old > key ? old : key;  // carry the larger one
+    if (key == kEmptyKey) return;
+  }
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -236,7 +257,9 @@ struct JoinArgs {
   const u32 *nf, *nfn, *of, *ofn, *nr, *nrn, *orv, *orn;
   const float* worst;
   u64* slots;
-  u32 S;
+  u32 S;     // slots per point (= nb * ways)
+  u32 nb;    // buckets per point
+  u32 ways;  // slots per bucket
   u64* counters;
   int DC;    // dims per staged chunk (multiple of 8)
   int DCP;   // smem row stride in floats (DCP/4 odd: conflict-free LDS.128)
@@ -368,15 +391,13 @@ __global__ __launch_bounds__(kJoinThreads) void k_join(JoinArgs a) {
             const float dist = __fsqrt_rn(acc[m][r][c]);
             ++my_pairs;
             if (dist < a.worst[u]) {
-              atomicMin(reinterpret_cast<unsigned long long*>(a.slots + (u64)u * a.S +
-                                                              slot_hash(u, v, a.S)),
-                        (unsigned long long)pack_key(dist, v));
+              offer(a.slots + (u64)u * a.S + (u64)bucket_hash(u, v, a.nb) * a.ways, a.ways,
+                    pack_key(dist, v));
               ++my_offers;
             }
             if (dist < a.worst[v]) {
-              atomicMin(reinterpret_cast<unsigned long long*>(a.slots + (u64)v * a.S +
-                                                              slot_hash(v, u, a.S)),
-                        (unsigned long long)pack_key(dist, u));
+              offer(a.slots + (u64)v * a.S + (u64)bucket_hash(v, u, a.nb) * a.ways, a.ways,
+                    pack_key(dist, u));
               ++my_offers;
             }
           }
@@ -603,7 +624,10 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   const u64 n = ds.n;
   const u32 k = p.k;
   const u32 B = bound_of(p.rho, k);
-  const u32 S = (u32)(p.candidate_capacity ? p.candidate_capacity : 2ull * k);
+  const u32 cap = (u32)(p.candidate_capacity ? p.candidate_capacity : 2ull * k);
+  const u32 ways = cap < kWays ? cap : kWays;
+  const u32 nb = cap / ways;
+  const u32 S = nb * ways;
   DeviceGuard guard(r.device);
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evb = nullptr, eve = nullptr;
@@ -647,6 +671,8 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   ja.worst = worst.p;
   ja.slots = slots.p;
   ja.S = S;
+  ja.nb = nb;
+  ja.ways = ways;
   ja.counters = counters.p;
   const int max_rows = (int)(2 * B + k + B);
   ja.RMAX = (max_rows + 3) & ~3;
