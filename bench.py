@@ -353,6 +353,8 @@ def main():
                             "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                             "algorithmic_bytes_per_launch": per_launch,
                             "avg_launch_ms": avg_ms, "join_share_of_step": st.join_ms / ms,
+                            "offer_kernel_ms_per_step": st.offer_ms,
+                            "offers_per_point": st.offers / n,
                             "sigma_per_point": st.pairs / n,
                             "staged_rows_per_point": st.staged_rows / n,
                             "iterations": st.iterations}

@@ -89,6 +89,7 @@ typedef struct {
   double total_ms;  /* device time of the whole build */
   uint64_t join_launches;
   uint64_t launches;
+  double offer_ms; /* device time of the offer (atomicMin cascade) kernel, summed */
 } knng_nnd_stats;
 
 /* SearchParams annsearch.hpp:12-19 */

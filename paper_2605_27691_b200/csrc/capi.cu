@@ -429,6 +429,7 @@ knng_status knng_nn_descent(knng_ctx* ctx, int device, const knng_dataset* ds,
       stats->join_ms = st.join_ms;
       stats->total_ms = st.total_ms;
       stats->join_launches = st.join_launches;
+      stats->offer_ms = st.offer_ms;
       stats->launches = st.launches + 1;
     }
   });

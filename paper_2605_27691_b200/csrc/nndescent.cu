@@ -16,7 +16,9 @@
 //                  so the build is deterministic regardless of scheduling.
 //   k_apply        warp per point: knn_insert of every surviving slot in slot
 //                  order (:199-223), gross accepted count, worst refresh.
+#include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "nndescent.hpp"
 
@@ -261,55 +263,109 @@ struct JoinArgs {
   u32 nb;    // buckets per point
   u32 ways;  // slots per bucket
   u64* counters;
+  u64 p_lo, p_hi;      // point slice of this launch
+  u64* q_key;          // offer queue: CTA c owns [c * q_per_cta, (c+1) * q_per_cta)
+  u32* q_tgt;
+  u32* q_fill;         // entries used per CTA region
+  u64 q_per_cta;
   int DC;    // dims per staged chunk (multiple of 8)
   int DCP;   // smem row stride in floats (DCP/4 odd: conflict-free LDS.128)
   int RMAX;  // smem rows (>= max list size, multiple of 4)
 };
 
-// Append the unique, not-yet-listed ids of src[0..len) to s_ids[*cnt..).
-__device__ __forceinline__ void warp_append_unique(u32* s_ids, int& cnt, const u32* src,
-                                                   u32 len) {
-  const unsigned lane = lane_id();
-  for (u32 base = 0; base < len; base += 32) {
-    const bool valid = base + lane < len;
-    const u32 c = valid ? src[base + lane] : kNone;
-    const unsigned m = __match_any_sync(kFull, c);
-    bool keep = valid && (__ffs(m) - 1 == (int)lane);
-    for (int t = 0; t < cnt; ++t) keep = keep && (s_ids[t] != c);
-    const unsigned b = __ballot_sync(kFull, keep);
-    if (keep) s_ids[cnt + __popc(b & lanemask_lt())] = c;
-    cnt += __popc(b);
-    __syncwarp();
+// Offers the join produced: every thread resolves one queued offer's
+// atomicMin cascade (full occupancy hides the L2 round trips the cascade
+// depends on).  Regions of CTAs that produced nothing are skipped.
+__global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
+                                               const u32* __restrict__ q_tgt,
+                                               const u32* __restrict__ q_fill, u64 q_per_cta,
+                                               u32 regions, u32 split, u64* __restrict__ slots,
+                                               u32 S, u32 nb, u32 ways) {
+  const u32 region = blockIdx.x / split, sub = blockIdx.x % split;
+  if (region >= regions) return;
+  const u32 fill = q_fill[region];
+  const u64 base = (u64)region * q_per_cta;
+  for (u32 e = sub * blockDim.x + threadIdx.x; e < fill; e += split * blockDim.x) {
+    const u64 key = q_key[base + e];
+    const u32 tgt = q_tgt[base + e];
+    offer(slots + (u64)tgt * S + (u64)bucket_hash(tgt, key_id(key), nb) * ways, ways, key);
   }
 }
 
-__global__ __launch_bounds__(kJoinThreads) void k_join(JoinArgs a) {
+// smem layout of one join CTA (dynamic):
+//   s_ids[RMAX] u32 | s_worst[RMAX] f32 | s_cand[RMAX] u32 | s_hash[256] u64 |
+//   s_int[16] | s_x[RMAX * DCP] f32 (feature tile)
+constexpr int kHashSlots = 256;
+
+__global__ __launch_bounds__(kJoinThreads, 4) void k_join(JoinArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   u32* s_ids = reinterpret_cast<u32*>(smem);
-  int* s_cnt = reinterpret_cast<int*>(smem + a.RMAX * 4);
-  float* s_x = reinterpret_cast<float*>(smem + a.RMAX * 4 + 16);
+  float* s_worst = reinterpret_cast<float*>(smem + a.RMAX * 4);
+  u32* s_cand = reinterpret_cast<u32*>(smem + a.RMAX * 8);
+  u64* s_hash = reinterpret_cast<u64*>(smem + a.RMAX * 12);
+  int* s_int = reinterpret_cast<int*>(smem + a.RMAX * 12 + kHashSlots * 8);
+  float* s_x = reinterpret_cast<float*>(smem + a.RMAX * 12 + kHashSlots * 8 + 64);
   const int tid = threadIdx.x;
-  const unsigned lane = lane_id();
+  const unsigned lane = lane_id(), warp = tid >> 5;
   const bool vec = (a.d & 3) == 0;
-  u64 my_pairs = 0, my_offers = 0, my_rows = 0, my_pts = 0;
+  u64 my_pairs = 0, my_rows = 0, my_pts = 0;
+  u64* qk = a.q_key + (u64)blockIdx.x * a.q_per_cta;
+  u32* qt = a.q_tgt + (u64)blockIdx.x * a.q_per_cta;
+  u32 q_used = 0;  // uniform across the CTA
 
-  for (u64 p = blockIdx.x; p < a.n; p += gridDim.x) {
-    __syncthreads();  // previous point's smem fully consumed
-    if (tid < 32) {
-      int nn = 0;
-      warp_append_unique(s_ids, nn, a.nf + p * a.B, a.nfn[p]);
-      warp_append_unique(s_ids, nn, a.nr + p * a.B, a.nrn[p]);
-      int na = nn;
-      warp_append_unique(s_ids, na, a.of + p * a.k, a.ofn[p]);
-      warp_append_unique(s_ids, na, a.orv + p * a.B, a.orn[p]);
-      if (lane == 0) {
-        s_cnt[0] = nn;
-        s_cnt[1] = na;
+  for (u64 p = a.p_lo + blockIdx.x; p < a.p_hi; p += gridDim.x) {
+    // ---- join lists (nndescent.cpp:135-153): new = nf U nr, old = (of U orv)
+    // \ new, first occurrence wins, order kept.  One candidate per thread;
+    // duplicates resolved through a smem hash of id -> smallest position.
+    const int a0 = a.nfn[p], a1 = a.nrn[p], a2 = a.ofn[p], a3 = a.orn[p];
+    const int tot = a0 + a1 + a2 + a3;
+    __syncthreads();  // previous point fully consumed
+    for (int t = tid; t < kHashSlots; t += kJoinThreads) s_hash[t] = kEmptyKey;
+    u32 c = kNone;
+    if (tid < tot) {
+      if (tid < a0) c = a.nf[p * a.B + tid];
+      else if (tid < a0 + a1) c = a.nr[p * a.B + (tid - a0)];
+      else if (tid < a0 + a1 + a2) c = a.of[p * a.k + (tid - a0 - a1)];
+      else c = a.orv[p * a.B + (tid - a0 - a1 - a2)];
+    }
+    __syncthreads();
+    u32 h = (c * 0x9E3779B1u) >> 24;  // 256 slots
+    const u64 mine = ((u64)c << 32) | (u32)tid;
+    if (tid < tot) {
+      while (true) {
+        const u64 old = atomicCAS(reinterpret_cast<unsigned long long*>(&s_hash[h]),
+                                  (unsigned long long)kEmptyKey, (unsigned long long)mine);
+        if (old == kEmptyKey || (u32)(old >> 32) == c) {
+          if (old != kEmptyKey) atomicMin(reinterpret_cast<unsigned long long*>(&s_hash[h]),
+                                          (unsigned long long)mine);
+          break;
+        }
+        h = (h + 1) & (kHashSlots - 1);
       }
     }
     __syncthreads();
-    const int nn = s_cnt[0], na = s_cnt[1];
-    if (nn == 0 || na < 2) continue;
+    const bool keep = tid < tot && s_hash[h] == mine;
+    const unsigned kb = __ballot_sync(kFull, keep);
+    const unsigned nbm = __ballot_sync(kFull, keep && tid < a0 + a1);
+    if (lane == 0) {
+      s_int[warp] = __popc(kb);
+      s_int[8 + warp] = __popc(nbm);
+    }
+    __syncthreads();
+    int base = 0, nn = 0, na = 0;
+#pragma unroll
+    for (int w = 0; w < kJoinThreads / 32; ++w) {
+      if (w < (int)warp) base += s_int[w];
+      na += s_int[w];
+      nn += s_int[8 + w];
+    }
+    if (nn == 0 || na < 2) continue;  // uniform: no pairs at this point
+    if (keep) {
+      const int pos = base + __popc(kb & lanemask_lt());
+      s_ids[pos] = c;
+      s_worst[pos] = a.worst[c];
+    }
+    __syncthreads();
     const int RT = (nn + 3) >> 2, CT = (na + 3) >> 2;
     const int ntiles = RT * CT;
     if (tid == 0) {
@@ -323,22 +379,21 @@ __global__ __launch_bounds__(kJoinThreads) void k_join(JoinArgs a) {
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[m][r][c] = 0.0f;
+          for (int cc = 0; cc < 4; ++cc) acc[m][r][cc] = 0.0f;
       for (int c0 = 0; c0 < a.d; c0 += a.DC) {
         const int dc = min(a.DC, a.d - c0);
-        __syncthreads();
+        if (c0 > 0 || pass > 0) __syncthreads();
         if (vec) {
           const int q = dc >> 2;
           for (int t = tid; t < na * q; t += kJoinThreads) {
             const int row = t / q, c4 = t - row * q;
-            cp_async16(s_x + row * a.DCP + c4 * 4,
-                       a.X + (u64)s_ids[row] * a.d + c0 + c4 * 4);
+            cp_async16(s_x + row * a.DCP + c4 * 4, a.X + (u64)s_ids[row] * a.d + c0 + c4 * 4);
           }
           cp_async_wait_all();
         } else {
           for (int t = tid; t < na * dc; t += kJoinThreads) {
-            const int row = t / dc, c = t - row * dc;
-            s_x[row * a.DCP + c] = a.X[(u64)s_ids[row] * a.d + c0 + c];
+            const int row = t / dc, cc = t - row * dc;
+            s_x[row * a.DCP + cc] = a.X[(u64)s_ids[row] * a.d + c0 + cc];
           }
         }
         __syncthreads();
@@ -353,69 +408,106 @@ __global__ __launch_bounds__(kJoinThreads) void k_join(JoinArgs a) {
 #pragma unroll
           for (int r = 0; r < 4; ++r) ra[r] = s_x + (ti + RT * r) * a.DCP;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) rb[c] = s_x + (tj + CT * c) * a.DCP;
+          for (int cc = 0; cc < 4; ++cc) rb[cc] = s_x + (tj + CT * cc) * a.DCP;
           for (int dd = 0; dd < dc4; dd += 4) {
             float4 va[4], vb[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) va[r] = *reinterpret_cast<const float4*>(ra[r] + dd);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) vb[c] = *reinterpret_cast<const float4*>(rb[c] + dd);
+            for (int cc = 0; cc < 4; ++cc) vb[cc] = *reinterpret_cast<const float4*>(rb[cc] + dd);
 #pragma unroll
             for (int r = 0; r < 4; ++r)
 #pragma unroll
-              for (int c = 0; c < 4; ++c) acc[m][r][c] = sq_step4(acc[m][r][c], va[r], vb[c]);
+              for (int cc = 0; cc < 4; ++cc)
+                acc[m][r][cc] = sq_step4(acc[m][r][cc], va[r], vb[cc]);
           }
           for (int dd = dc4; dd < dc; ++dd) {
 #pragma unroll
             for (int r = 0; r < 4; ++r)
 #pragma unroll
-              for (int c = 0; c < 4; ++c) acc[m][r][c] = sq_step(acc[m][r][c], ra[r][dd], rb[c][dd]);
+              for (int cc = 0; cc < 4; ++cc)
+                acc[m][r][cc] = sq_step(acc[m][r][cc], ra[r][dd], rb[cc][dd]);
           }
         }
       }
-      // offers: (u, v, sigma) to both endpoints (nndescent.cpp:160-171)
+      // ---- offers (nndescent.cpp:160-171): worst filter against the staged
+      // snapshot; survivors appended to this CTA's queue region in HBM
+      u32 pass_mask[kTPT];
+      int my_q = 0;
 #pragma unroll
       for (int m = 0; m < kTPT; ++m) {
+        pass_mask[m] = 0;
         const int t = pass + tid + m * kJoinThreads;
         if (t >= ntiles) continue;
         const int ti = t / CT, tj = t - ti * CT;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int i = ti + RT * r;
-          if (i >= nn) continue;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int j = tj + CT * c;
-            if (j >= na || j <= i) continue;
-            const u32 u = s_ids[i], v = s_ids[j];
-            const float dist = __fsqrt_rn(acc[m][r][c]);
+          for (int cc = 0; cc < 4; ++cc) {
+            const int j = tj + CT * cc;
+            if (i >= nn || j >= na || j <= i) continue;
+            const float dist = __fsqrt_rn(acc[m][r][cc]);
+            acc[m][r][cc] = dist;
             ++my_pairs;
-            if (dist < a.worst[u]) {
-              offer(a.slots + (u64)u * a.S + (u64)bucket_hash(u, v, a.nb) * a.ways, a.ways,
-                    pack_key(dist, v));
-              ++my_offers;
-            }
-            if (dist < a.worst[v]) {
-              offer(a.slots + (u64)v * a.S + (u64)bucket_hash(v, u, a.nb) * a.ways, a.ways,
-                    pack_key(dist, u));
-              ++my_offers;
+            const int bit = (r * 4 + cc) * 2;
+            if (dist < s_worst[i]) pass_mask[m] |= 1u << bit;
+            if (dist < s_worst[j]) pass_mask[m] |= 2u << bit;
+          }
+        }
+        my_q += __popc(pass_mask[m]);
+      }
+      // block-wide exclusive prefix of the per-thread offer counts
+      int incl = my_q;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if ((int)lane >= o) incl += y;
+      }
+      if (lane == 31) s_int[warp] = incl;
+      __syncthreads();
+      int wbase = 0, btot = 0;
+#pragma unroll
+      for (int w = 0; w < kJoinThreads / 32; ++w) {
+        if (w < (int)warp) wbase += s_int[w];
+        btot += s_int[w];
+      }
+      u64 slot = q_used + wbase + incl - my_q;
+      q_used += btot;
+#pragma unroll
+      for (int m = 0; m < kTPT; ++m) {
+        const u32 pm = pass_mask[m];
+        if (!pm) continue;
+        const int t = pass + tid + m * kJoinThreads;
+        const int ti = t / CT, tj = t - ti * CT;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const u32 two = (pm >> ((r * 4 + cc) * 2)) & 3u;
+            if (!two) continue;
+            const u32 u = s_ids[ti + RT * r], v = s_ids[tj + CT * cc];
+            const float dist = acc[m][r][cc];
+#pragma unroll
+            for (int dir = 0; dir < 2; ++dir) {
+              if (!((two >> dir) & 1u)) continue;
+              qk[slot] = pack_key(dist, dir ? u : v);
+              qt[slot] = dir ? v : u;
+              ++slot;
             }
           }
         }
       }
     }
   }
+  if (tid == 0) a.q_fill[blockIdx.x] = q_used;
   // one atomic per warp for the device counters
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    my_pairs += __shfl_xor_sync(kFull, my_pairs, o);
-    my_offers += __shfl_xor_sync(kFull, my_offers, o);
-  }
-  if (lane == 0) {
+  for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(kFull, my_pairs, o);
+  if (lane == 0)
     atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntPairs), my_pairs);
-    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntOffers), my_offers);
-  }
   if (tid == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntOffers), (u64)q_used);
     atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntStagedRows), my_rows);
     atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntJoinPoints), my_pts);
   }
@@ -678,7 +770,7 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   ja.RMAX = (max_rows + 3) & ~3;
   ja.DC = ds.d <= 128 ? ((ds.d + 7) & ~7) : 128;
   ja.DCP = ja.DC + 4;  // DC % 8 == 0 -> (DCP/4) odd
-  const size_t smem = (size_t)ja.RMAX * 4 + 16 + (size_t)ja.RMAX * ja.DCP * 4;
+  const size_t smem = (size_t)ja.RMAX * 12 + kHashSlots * 8 + 64 + (size_t)ja.RMAX * ja.DCP * 4;
   KNNG_CUDA(cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
   int per_sm = 0;
@@ -686,20 +778,56 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   if (per_sm < 1) per_sm = 1;
   const unsigned jgrid = persistent_grid(r, per_sm, n);
 
+  // Offer queue: each join CTA owns a region sized for the worst case of its
+  // points (2 offers per pair, max pairs C(2B,2) + 2B(k+B)), so nothing can
+  // overflow; points are processed in slices to bound the queue to ~4 GB.
+  const u64 nn_max = 2ull * B, no_max = (u64)k + B;
+  const u64 max_offers_pp = 2 * (nn_max * (nn_max - 1) / 2 + nn_max * no_max);
+  size_t free_b = 0, total_b = 0;
+  KNNG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const u64 budget = std::min<u64>(4ull << 30, free_b / 4);
+  u64 slice = budget / (max_offers_pp * 12);
+  slice = std::max<u64>(slice / jgrid, 1) * jgrid;
+  if (slice > n) slice = n;
+  const u64 q_per_cta = ceil_div<u64>(slice, jgrid) * max_offers_pp;
+  DBuf<u64> q_key(r, q_per_cta * jgrid);
+  DBuf<u32> q_tgt(r, q_per_cta * jgrid), q_fill(r, jgrid);
+  ja.q_key = q_key.p;
+  ja.q_tgt = q_tgt.p;
+  ja.q_fill = q_fill.p;
+  ja.q_per_cta = q_per_cta;
+  constexpr u32 kOfferSplit = 8;
+  const u64 nslices = ceil_div<u64>(n, slice);
+  std::vector<cudaEvent_t> sev;
+  if (time_kernels) {
+    sev.resize(3 * nslices);
+    for (auto& e : sev) KNNG_CUDA(cudaEventCreate(&e));
+  }
+
   if (st) *st = NndStats{};
   const double threshold = p.delta * (double)k * (double)n;
   for (u64 iter = 0; iter < p.max_iters; ++iter) {
     counters.zero();
     const u64 iter_seed = mix_seed(p.seed, 0x5a3f1e00ull + iter);
     sample_into(r, n, k, B, iter_seed, keys, flags, s, c, &launches);
-    if (time_kernels) KNNG_CUDA(cudaEventRecord(ev0, r.stream));
-    k_join<<<jgrid, kJoinThreads, smem, r.stream>>>(ja);
-    KNNG_LAUNCH_CHECK();
-    if (time_kernels) KNNG_CUDA(cudaEventRecord(ev1, r.stream));
+    for (u64 si = 0; si < nslices; ++si) {
+      ja.p_lo = si * slice;
+      ja.p_hi = std::min<u64>(n, ja.p_lo + slice);
+      if (time_kernels) KNNG_CUDA(cudaEventRecord(sev[3 * si], r.stream));
+      k_join<<<jgrid, kJoinThreads, smem, r.stream>>>(ja);
+      KNNG_LAUNCH_CHECK();
+      if (time_kernels) KNNG_CUDA(cudaEventRecord(sev[3 * si + 1], r.stream));
+      k_offer<<<jgrid * kOfferSplit, 256, 0, r.stream>>>(q_key.p, q_tgt.p, q_fill.p, q_per_cta,
+                                                          jgrid, kOfferSplit, slots.p, S, nb,
+                                                          ways);
+      KNNG_LAUNCH_CHECK();
+      if (time_kernels) KNNG_CUDA(cudaEventRecord(sev[3 * si + 2], r.stream));
+      launches += 2;
+    }
     k_apply<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst.p, slots.p,
                                                    counters.p);
     KNNG_LAUNCH_CHECK();
-    launches += 2;
+    launches += 1;
     KNNG_CUDA(cudaMemcpyAsync(hcount.p, counters.p, kNumCounters * sizeof(u64),
                               cudaMemcpyDeviceToHost, r.stream));
     r.sync();
@@ -711,10 +839,14 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
       st->staged_rows += hcount.p[kCntStagedRows];
       st->offers += hcount.p[kCntOffers];
       if (time_kernels) {
-        float ms = 0;
-        KNNG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-        st->join_ms += ms;
-        st->join_launches += 1;
+        for (u64 si = 0; si < nslices; ++si) {
+          float ms = 0;
+          KNNG_CUDA(cudaEventElapsedTime(&ms, sev[3 * si], sev[3 * si + 1]));
+          st->join_ms += ms;
+          KNNG_CUDA(cudaEventElapsedTime(&ms, sev[3 * si + 1], sev[3 * si + 2]));
+          st->offer_ms += ms;
+          st->join_launches += 1;
+        }
       }
     }
     if ((double)accepted < threshold) break;
@@ -729,6 +861,7 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
     cudaEventDestroy(ev1);
     cudaEventDestroy(evb);
     cudaEventDestroy(eve);
+    for (auto& e : sev) cudaEventDestroy(e);
   }
   if (st) st->launches = launches;
 }

@@ -44,6 +44,7 @@ struct NndStats {
   // Device time of the join kernel summed over iterations (CUDA events on the
   // launching stream) and of the whole build.
   double join_ms = 0.0;
+  double offer_ms = 0.0;  // k_offer (atomicMin cascades), summed
   double total_ms = 0.0;
   uint64_t join_launches = 0;
   uint64_t launches = 0;  // all kernels launched by the build

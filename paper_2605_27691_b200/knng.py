@@ -88,7 +88,7 @@ class _NndStats(C.Structure):
                 ("accepted_cap", C.c_uint64), ("pairs", C.c_uint64),
                 ("staged_rows", C.c_uint64), ("offers", C.c_uint64), ("join_ms", C.c_double),
                 ("total_ms", C.c_double), ("join_launches", C.c_uint64),
-                ("launches", C.c_uint64)]
+                ("launches", C.c_uint64), ("offer_ms", C.c_double)]
 
 
 class _SearchParams(C.Structure):
@@ -314,6 +314,7 @@ class NnDescentStats:
     staged_rows: int = 0
     offers: int = 0
     join_ms: float = 0.0
+    offer_ms: float = 0.0
     total_ms: float = 0.0
     join_launches: int = 0
     launches: int = 0
@@ -562,7 +563,7 @@ def nn_descent(x, params: Optional[NnDescentParams] = None, stats: Optional[NnDe
         stats.iterations = st.iterations
         stats.accepted_per_iter = [int(v) for v in acc[:st.iterations]]
         stats.pairs, stats.staged_rows, stats.offers = st.pairs, st.staged_rows, st.offers
-        stats.join_ms, stats.total_ms = st.join_ms, st.total_ms
+        stats.join_ms, stats.total_ms, stats.offer_ms = st.join_ms, st.total_ms, st.offer_ms
         stats.join_launches, stats.launches = st.join_launches, st.launches
     return g
 
