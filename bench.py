@@ -355,6 +355,9 @@ def main():
                             "avg_launch_ms": avg_ms, "join_share_of_step": st.join_ms / ms,
                             "offer_kernel_ms_per_step": st.offer_ms,
                             "offers_per_point": st.offers / n,
+                            "stage_ms_per_step": st.stage_ms, "build_device_ms": st.total_ms,
+                            "offers_per_iter": st.offers_per_iter,
+                            "pairs_per_iter": st.pairs_per_iter,
                             "sigma_per_point": st.pairs / n,
                             "staged_rows_per_point": st.staged_rows / n,
                             "iterations": st.iterations}

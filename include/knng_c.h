@@ -90,6 +90,11 @@ typedef struct {
   uint64_t join_launches;
   uint64_t launches;
   double offer_ms; /* device time of the offer (atomicMin cascade) kernel, summed */
+  /* device time per stage (ms): init, sample, join lists, join, offer, apply,
+   * readback + host gaps, unused */
+  double stage_ms[8];
+  uint64_t* offers_per_iter; /* caller arrays of accepted_cap entries, nullable */
+  uint64_t* pairs_per_iter;
 } knng_nnd_stats;
 
 /* SearchParams annsearch.hpp:12-19 */

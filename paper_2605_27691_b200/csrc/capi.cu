@@ -2,6 +2,9 @@
 // never cross it: each entry point maps the reference's exception classes to
 // a status code and keeps e.what() for knng_last_error().
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -40,6 +43,25 @@ struct knng_ctx {
 namespace {
 
 thread_local std::string g_err;
+
+// KNNG_TRACE=1: host timestamps of the phases of a C-ABI call on stderr.
+struct HostTrace {
+  const char* name;
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  explicit HostTrace(const char* n) : name(n), on(std::getenv("KNNG_TRACE") != nullptr) {
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[knng %s] %s %.3f ms (total %.3f)\n", name, what,
+                 std::chrono::duration<double, std::milli>(t - last).count(),
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    last = t;
+  }
+  ~HostTrace() { mark("exit"); }
+};
 
 template <class F>
 knng_status guard(F&& f) {
@@ -396,13 +418,16 @@ knng_status knng_nn_descent(knng_ctx* ctx, int device, const knng_dataset* ds,
     check_ds(ds);
     validate_nnd(p, ds->n);
     require(out->n == ds->n && out->k == p.k, "nn_descent: output shape mismatch");
+    HostTrace tr("nn_descent");
     DevData x;
     stage(r, ds, x);
     const u64 n = ds->n, k = p.k;
     DBuf<u64> keys(r, n * k);
     DBuf<u32> flags(r, n);
     NndStats st;
+    tr.mark("alloc");
     nn_descent_device(r, DevRows{x.p, n, (int)ds->dims}, p, keys.p, flags.p, &st, stats != nullptr);
+    tr.mark("build");
     const bool dev = out->mem == KNNG_MEM_DEVICE;
     if (dev) {
       export_graph_device(r, keys.p, flags.p, n, (u32)k, 0, out->ids, out->dists, out->flags);
@@ -430,6 +455,11 @@ knng_status knng_nn_descent(knng_ctx* ctx, int device, const knng_dataset* ds,
       stats->total_ms = st.total_ms;
       stats->join_launches = st.join_launches;
       stats->offer_ms = st.offer_ms;
+      for (int i = 0; i < 8; ++i) stats->stage_ms[i] = st.stage_ms[i];
+      for (u64 i = 0; i < std::min<u64>(stats->accepted_cap, st.offers_per_iter.size()); ++i) {
+        if (stats->offers_per_iter) stats->offers_per_iter[i] = st.offers_per_iter[i];
+        if (stats->pairs_per_iter) stats->pairs_per_iter[i] = st.pairs_per_iter[i];
+      }
       stats->launches = st.launches + 1;
     }
   });

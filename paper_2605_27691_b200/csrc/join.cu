@@ -1,0 +1,684 @@
+// join.cu -- NN-Descent local join (nndescent.cpp:135-197) on the B200.
+//
+//   k_join_lists  warp per point: build_join_lists (:135-153) -- new = nf U nr,
+//                 old = (of U orv) \ new, first occurrence wins -- written
+//                 compactly (L_ids[p * RMAX ..], L_cnt[p] = nn | na << 16).
+//   k_join        one persistent CTA per SM, a software pipeline over batches
+//                 of points: while batch b is computed from one smem buffer,
+//                 the feature rows of batch b+1 stream into the other with
+//                 cp.async (16 B, coalesced per row).  A batch packs as many
+//                 points as fit (~175 rows of 128-d); its 4x4 micro-tiles --
+//                 a triangle of new x new blocks plus the new x old rectangle
+//                 of every point, rows interleaved so consecutive threads read
+//                 consecutive smem rows (conflict-free LDS.128) -- are spread
+//                 over all 256 threads.  Distances are exact-order (common.cuh),
+//                 filtered by the worst snapshot (nndescent.hpp:39-40) and the
+//                 survivors appended to the chunk's offer queue in HBM.
+//   k_offer       resolves queued offers into the 4-way candidate buckets with
+//                 atomicMin cascades (lock-free, order-independent).
+#include <algorithm>
+
+#include "join.hpp"
+#include "nndescent.hpp"
+
+namespace knng_b200 {
+namespace {
+
+constexpr u32 kNone = 0xffffffffu;
+constexpr int kJT = 512;                // threads per join CTA
+constexpr int kTPT = 1;                 // micro-tiles per thread
+constexpr int kMaxTiles = kJT * kTPT;   // tiles per batch
+constexpr int G = kJoinChunk;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Bucket of candidate v in point u's candidate buffer (kWays slots each).
+__device__ __forceinline__ u32 bucket_hash(u32 u, u32 v, u32 nb) {
+  u32 x = v * 0x9E3779B1u + u * 0x85EBCA77u;
+  x ^= x >> 15;
+  x *= 0x2C1B3C6Du;
+  x ^= x >> 12;
+  x *= 0x297A2D39u;
+  x ^= x >> 15;
+  return x % nb;
+}
+
+// Lock-free offer given a snapshot of its bucket.  The bucket keeps its W
+// smallest distinct (dist,id) keys in ascending order: each step atomicMin's
+// the carried key into one slot and carries the larger of (old, key) onward.
+// Slots only decrease, so whatever the interleaving the final bucket is the W
+// smallest distinct keys offered (order-independent -> deterministic build).
+// Any snapshot is safe: a key >= the snapshot tail can never be among the W
+// smallest, a key equal to a snapshot entry is already buffered (or displaced
+// by smaller ones), and every slot before the snapshot insertion position
+// already holds a smaller key, so the cascade starts there.
+__device__ __forceinline__ void offer_from(u64* __restrict__ bucket, u32 ways, u64 key,
+                                           const u64 (&snap)[4]) {
+  u32 pos = 0;
+#pragma unroll
+  for (u32 w = 0; w < 4; ++w) {
+    if (w < ways && snap[w] == key) return;
+    pos += (w < ways && snap[w] < key) ? 1u : 0u;
+  }
+  if (pos >= ways) return;
+  for (u32 w = pos; w < ways; ++w) {
+    const u64 old = atomicMin(reinterpret_cast<unsigned long long*>(bucket + w),
+                              (unsigned long long)key);
+    if (old == key) return;
+    key = old > key ? old : key;
+    if (key == kEmptyKey) return;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_join_lists
+// ---------------------------------------------------------------------------
+__global__ __launch_bounds__(256) void k_join_lists(u64 n, u32 k, u32 B, int RMAX,
+                                                    const u32* __restrict__ nf,
+                                                    const u32* __restrict__ nfn,
+                                                    const u32* __restrict__ of,
+                                                    const u32* __restrict__ ofn,
+                                                    const u32* __restrict__ nr,
+                                                    const u32* __restrict__ nrn,
+                                                    const u32* __restrict__ orv,
+                                                    const u32* __restrict__ orn,
+                                                    u32* __restrict__ L_ids,
+                                                    u32* __restrict__ L_cnt) {
+  __shared__ u32 s_list[8][128];
+  const unsigned lane = lane_id(), w = threadIdx.x >> 5;
+  u32* lst = s_list[w];
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + w; p < n; p += warps) {
+    int cnt = 0, nn = 0;
+    for (int src = 0; src < 4; ++src) {
+      const u32* base = src == 0 ? nf + p * B : src == 1 ? nr + p * B : src == 2 ? of + p * k
+                                                                                 : orv + p * B;
+      const u32 len = src == 0 ? nfn[p] : src == 1 ? nrn[p] : src == 2 ? ofn[p] : orn[p];
+      for (u32 b0 = 0; b0 < len; b0 += 32) {
+        const bool valid = b0 + lane < len;
+        const u32 c = valid ? base[b0 + lane] : kNone;
+        const unsigned m = __match_any_sync(kFull, c);
+        bool keep = valid && (__ffs(m) - 1 == (int)lane);
+        for (int t = 0; t < cnt && keep; ++t) keep = lst[t] != c;
+        const unsigned kb = __ballot_sync(kFull, keep);
+        if (keep) lst[cnt + __popc(kb & lanemask_lt())] = c;
+        cnt += __popc(kb);
+        __syncwarp();
+      }
+      if (src == 1) nn = cnt;
+    }
+    for (int t = lane; t < cnt; t += 32) L_ids[p * RMAX + t] = lst[t];
+    if (lane == 0) L_cnt[p] = (u32)nn | ((u32)cnt << 16);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_offer
+// ---------------------------------------------------------------------------
+constexpr int kOfferBatch = 4;
+
+__global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
+                                               const u32* __restrict__ q_tgt,
+                                               const u32* __restrict__ q_fill, u64 q_per_chunk,
+                                               u32 chunks, u64* __restrict__ slots, u32 S,
+                                               u32 nb, u32 ways, u64* __restrict__ counters) {
+  for (u32 region = blockIdx.x; region < chunks; region += gridDim.x) {
+    const u32 fill = q_fill[region];
+    if (threadIdx.x == 0 && counters)
+      atomicAdd(reinterpret_cast<unsigned long long*>(counters + kCntOfferSeen), (u64)fill);
+    const u64 base = (u64)region * q_per_chunk;
+    // warp-uniform trip count + __syncwarp: lanes that leave the cascade early
+    // must not race ahead, or the warp splits into 1-2-lane groups
+    for (u32 e_base = 0; e_base < fill; e_base += kOfferBatch * blockDim.x) {
+      const u32 e0 = e_base + threadIdx.x;
+      u64 key[kOfferBatch];
+      u64* bk[kOfferBatch];
+      u64 snap[kOfferBatch][4];
+#pragma unroll
+      for (int i = 0; i < kOfferBatch; ++i) {
+        const u32 e = e0 + i * blockDim.x;
+        bk[i] = nullptr;
+        if (e < fill) {
+          key[i] = q_key[base + e];
+          const u32 tgt = q_tgt[base + e];
+          bk[i] = slots + (u64)tgt * S + (u64)bucket_hash(tgt, key_id(key[i]), nb) * ways;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kOfferBatch; ++i) {
+        if (!bk[i]) continue;
+        if (ways == 4) {
+          // L2-coherent snapshot (L1 lines would go stale under the atomics)
+          const ulonglong2 lo = __ldcg(reinterpret_cast<const ulonglong2*>(bk[i]));
+          const ulonglong2 hi = __ldcg(reinterpret_cast<const ulonglong2*>(bk[i] + 2));
+          snap[i][0] = lo.x;
+          snap[i][1] = lo.y;
+          snap[i][2] = hi.x;
+          snap[i][3] = hi.y;
+        } else {
+#pragma unroll
+          for (u32 w = 0; w < 4; ++w) snap[i][w] = w < ways ? __ldcg(bk[i] + w) : kEmptyKey;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kOfferBatch; ++i)
+        if (bk[i]) offer_from(bk[i], ways, key[i], snap[i]);
+      __syncwarp();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_join
+// ---------------------------------------------------------------------------
+struct JoinArgs {
+  const float* X;
+  int d;
+  const u32* L_ids;
+  const u32* L_cnt;
+  int RMAX;
+  const float* worst;
+  u64 p_lo, p_hi;
+  u32* chunk_counter;
+  u64* q_key;
+  u32* q_tgt;
+  u32* q_fill;
+  u64 q_per_chunk;
+  int DC, DCP, RB;
+  u64* counters;
+};
+
+__device__ __forceinline__ int tri_count(int rt) { return rt * (rt + 1) / 2; }
+__device__ __forceinline__ int tiles_of(u32 cnt) {
+  const int nn = cnt & 0xffff, na = cnt >> 16;
+  const int rt = (nn + 3) >> 2, cto = (na - nn + 3) >> 2;
+  return (nn == 0 || na < 2) ? 0 : tri_count(rt) + rt * cto;
+}
+
+// A 4x4 micro-tile of one point: rows = new entries ti + RT*r, columns = new
+// entries tj + RT*c (triangle part) or old entries tj + CTo*c (rectangle).
+struct Tile {
+  int pt;          // point slot in the chunk (-1: none)
+  int row0, rstr;  // batch smem row of row 0, stride
+  int col0, cstr;  // batch smem row of column 0, stride
+  int nn, no;
+  int ti, tj;
+  bool tri;
+};
+
+// per meta slot (2): s_ids[G*RMAX] u32 | s_worst[G*RMAX] f32 | s_cnt[G] | hdr[4]
+// per desc slot (2): s_rb[G+1] | s_tb[G+1] | hdr[4]
+// misc[16] | x[2][(RB+4)*DCP]
+// Slots are addressed arithmetically (base + slot * stride) so nothing lands
+// in local memory.
+struct Smem {
+  unsigned char* meta;  // slot m at meta + m * meta_bytes
+  unsigned char* desc;  // slot q at desc + q * desc_bytes
+  int* misc;            // [0..15] warp sums, [16] chunk grab
+  float* x0;            // buffer b at x0 + b * xstride
+  int RMAX;
+  u32 meta_bytes, desc_bytes, xstride;
+  __device__ u32* ids(int m) const { return reinterpret_cast<u32*>(meta + m * meta_bytes); }
+  __device__ float* worst(int m) const {
+    return reinterpret_cast<float*>(meta + m * meta_bytes + G * RMAX * 4);
+  }
+  __device__ u32* cnt(int m) const {
+    return reinterpret_cast<u32*>(meta + m * meta_bytes + G * RMAX * 8);
+  }
+  __device__ int* mhdr(int m) const {  // [0] chunk, [1] np
+    return reinterpret_cast<int*>(meta + m * meta_bytes + G * RMAX * 8 + G * 4);
+  }
+  __device__ int* rb(int q) const { return reinterpret_cast<int*>(desc + q * desc_bytes); }
+  __device__ int* tb(int q) const { return rb(q) + (G + 1); }
+  __device__ int* dhdr(int q) const { return rb(q) + 2 * (G + 1); }  // [0] meta, [1] jb, [2] je
+  __device__ u32* rowid(int q) const { return reinterpret_cast<u32*>(rb(q) + 2 * (G + 1) + 4); }
+  __device__ float* x(int b) const { return x0 + b * xstride; }
+};
+
+__host__ __device__ inline size_t desc_slot_bytes(int RB) {
+  return ((size_t)(2 * (G + 1) + 4) * 4 + (size_t)RB * 4 + 15) & ~size_t(15);
+}
+
+__device__ __forceinline__ Smem carve(unsigned char* base, int RMAX, int RB, int DCP) {
+  Smem s;
+  s.RMAX = RMAX;
+  s.meta_bytes = (u32)((size_t)G * RMAX * 8 + G * 4 + 16);
+  s.desc_bytes = (u32)desc_slot_bytes(RB);
+  s.meta = base;
+  s.desc = base + 2 * s.meta_bytes;
+  s.misc = reinterpret_cast<int*>(s.desc + 2 * s.desc_bytes);
+  size_t off = 2 * (size_t)s.meta_bytes + 2 * (size_t)s.desc_bytes + 128;
+  off = (off + 15) & ~size_t(15);
+  s.x0 = reinterpret_cast<float*>(base + off);
+  s.xstride = (u32)((RB + 4) * DCP);
+  return s;
+}
+
+__host__ __device__ inline size_t join_smem_bytes(int RMAX, int RB, int DCP) {
+  size_t off = 2 * ((size_t)G * RMAX * 8 + G * 4 + 16) + 2 * desc_slot_bytes(RB) + 128;
+  off = (off + 15) & ~size_t(15);
+  return off + 2 * (size_t)(RB + 4) * DCP * 4;
+}
+
+// Grab the next chunk into meta slot m; returns false when the slice is done.
+__device__ bool load_chunk(const JoinArgs& a, const Smem& s, int m) {
+  const int tid = threadIdx.x;
+  __syncthreads();  // slot m is no longer read by anyone
+  if (tid == 0) s.misc[16] = (int)atomicAdd(a.chunk_counter, 1u);
+  __syncthreads();
+  const u32 chunk = (u32)s.misc[16];
+  const u64 p0 = a.p_lo + (u64)chunk * G;
+  if (p0 >= a.p_hi) return false;
+  const int np = (a.p_hi - p0) < (u64)G ? (int)(a.p_hi - p0) : G;
+  if (tid < np) s.cnt(m)[tid] = a.L_cnt[p0 + tid];
+  for (int e = tid; e < np * a.RMAX; e += kJT) {
+    const int j = e / a.RMAX, i = e - j * a.RMAX;
+    if (i < (int)(a.L_cnt[p0 + j] >> 16)) {
+      const u32 id = a.L_ids[(p0 + j) * a.RMAX + i];
+      s.ids(m)[e] = id;
+      s.worst(m)[e] = a.worst[id];
+    }
+  }
+  if (tid == 0) {
+    s.mhdr(m)[0] = (int)chunk;
+    s.mhdr(m)[1] = np;
+  }
+  __syncthreads();
+  return true;
+}
+
+// Thread 0 packs points [jb, ..) of meta slot m into desc slot q.
+__device__ void form_batch(const JoinArgs& a, const Smem& s, int q, int m, int jb) {
+  if (threadIdx.x == 0) {
+    const int np = s.mhdr(m)[1];
+    int rows = 0, tiles = 0, je = jb;
+    while (je < np) {
+      const u32 c = s.cnt(m)[je];
+      const int t = tiles_of(c);
+      const int na = t ? (int)(c >> 16) : 0;
+      if (je > jb && (rows + na > a.RB || tiles + t > kMaxTiles)) break;
+      s.rb(q)[je] = rows;
+      s.tb(q)[je] = tiles;
+      rows += na;
+      tiles += t;
+      ++je;
+    }
+    s.rb(q)[je] = rows;
+    s.tb(q)[je] = tiles;
+    s.dhdr(q)[0] = m;
+    s.dhdr(q)[1] = jb;
+    s.dhdr(q)[2] = je;
+  }
+}
+
+// Stage dims [c0, c0+dc) of every row of desc q into buffer buf (async).
+// Row -> point id table of desc q (all threads; once per batch).  Row r
+// belongs to the last point j with rb[j] <= r (zero-row points share rb).
+__device__ void fill_rowids(const JoinArgs& a, const Smem& s, int q) {
+  const int m = s.dhdr(q)[0], jb = s.dhdr(q)[1], je = s.dhdr(q)[2];
+  const int* rb = s.rb(q);
+  const int rows = rb[je];
+  u32* rowid = s.rowid(q);
+  for (int r = threadIdx.x; r < rows; r += kJT) {
+    int lo = jb, hi = je - 1;  // last j in [jb, je) with rb[j] <= r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rb[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    rowid[r] = s.ids(m)[lo * a.RMAX + (r - rb[lo])];
+  }
+}
+
+// Stage dims [c0, c0+dc) of every row of desc q into buffer buf (async,
+// one 16-byte cp.async per thread per step, all lanes busy).
+__device__ void issue_rows(const JoinArgs& a, const Smem& s, int q, int c0, int buf) {
+  const int je = s.dhdr(q)[2];
+  const int rows = s.rb(q)[je];
+  const int dc = min(a.DC, a.d - c0);
+  const u32* rowid = s.rowid(q);
+  float* xb = s.x(buf);
+  if ((a.d & 3) == 0) {
+    const int qd = dc >> 2;
+    for (int e = threadIdx.x; e < rows * qd; e += kJT) {
+      const int r = e / qd, c4 = e - r * qd;
+      cp_async16(xb + r * a.DCP + c4 * 4, a.X + (u64)rowid[r] * a.d + c0 + c4 * 4);
+    }
+  } else {
+    for (int e = threadIdx.x; e < rows * dc; e += kJT) {
+      const int r = e / dc, cc = e - r * dc;
+      xb[r * a.DCP + cc] = a.X[(u64)rowid[r] * a.d + c0 + cc];
+    }
+  }
+  cp_async_commit();
+}
+
+__device__ __forceinline__ Tile decode_tile(const Smem& s, int q, int t) {
+  Tile T;
+  const int m = s.dhdr(q)[0], jb = s.dhdr(q)[1], je = s.dhdr(q)[2];
+  if (t >= s.tb(q)[je]) {
+    T.pt = -1;
+    return T;
+  }
+  int j = jb;
+  while (j + 1 < je && s.tb(q)[j + 1] <= t) ++j;
+  const u32 c = s.cnt(m)[j];
+  const int nn = c & 0xffff, na = c >> 16;
+  const int rt = (nn + 3) >> 2, no = na - nn, cto = (no + 3) >> 2;
+  int lt = t - s.tb(q)[j];
+  T.pt = j;
+  T.nn = nn;
+  T.no = no;
+  T.rstr = rt;
+  if (lt < tri_count(rt)) {
+    int ti = 0;
+    while (lt >= rt - ti) {
+      lt -= rt - ti;
+      ++ti;
+    }
+    T.tri = true;
+    T.ti = ti;
+    T.tj = ti + lt;
+    T.row0 = s.rb(q)[j] + ti;
+    T.col0 = s.rb(q)[j] + T.tj;
+    T.cstr = rt;
+  } else {
+    lt -= tri_count(rt);
+    T.tri = false;
+    T.ti = lt / cto;
+    T.tj = lt - T.ti * cto;
+    T.row0 = s.rb(q)[j] + T.ti;
+    T.col0 = s.rb(q)[j] + nn + T.tj;
+    T.cstr = cto;
+  }
+  return T;
+}
+
+__global__ __launch_bounds__(kJT, 1) void k_join(JoinArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Smem s = carve(smem, a.RMAX, a.RB, a.DCP);
+  const int tid = threadIdx.x;
+  const unsigned lane = lane_id(), warp = tid >> 5;
+  u64 my_pairs = 0, my_rows = 0, my_offers = 0;
+  u32 q_used0 = 0, q_used1 = 0;  // offers queued per meta slot (uniform)
+
+  // prologue: first chunk, first batch, first dim chunk
+  if (!load_chunk(a, s, 0)) return;
+  int cq = 0, cc0 = 0, cbuf = 0;  // current unit: desc slot, dim offset, buffer
+  form_batch(a, s, 0, 0, 0);
+  __syncthreads();
+  fill_rowids(a, s, 0);
+  __syncthreads();
+  issue_rows(a, s, 0, 0, 0);
+
+  Tile T[kTPT];
+  float acc[kTPT][4][4];
+  while (true) {
+    // ---- next unit: next dim chunk of this batch, next batch, or next chunk
+    int nq = cq, nc0 = cc0 + a.DC, nbuf = cbuf ^ 1;
+    bool have_next = true;
+    if (nc0 >= a.d) {
+      nc0 = 0;
+      nq = cq ^ 1;
+      const int m = s.dhdr(cq)[0];
+      const int je = s.dhdr(cq)[2];
+      if (je < s.mhdr(m)[1]) {
+        form_batch(a, s, nq, m, je);
+      } else if (load_chunk(a, s, m ^ 1)) {
+        if (m ^ 1) q_used1 = 0; else q_used0 = 0;
+        form_batch(a, s, nq, m ^ 1, 0);
+      } else {
+        have_next = false;
+      }
+      __syncthreads();
+      if (have_next) {
+        fill_rowids(a, s, nq);
+        __syncthreads();
+      }
+    }
+    if (have_next) {
+      issue_rows(a, s, nq, nc0, nbuf);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // current buffer landed for everyone
+
+    // ---- compute the current unit
+    const int m = s.dhdr(cq)[0];
+    if (cc0 == 0) {
+#pragma unroll
+      for (int t = 0; t < kTPT; ++t) T[t] = decode_tile(s, cq, tid + t * kJT);
+#pragma unroll
+      for (int t = 0; t < kTPT; ++t)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[t][r][c] = 0.0f;
+      if (tid == 0) my_rows += (u64)s.rb(cq)[s.dhdr(cq)[2]];
+    }
+    {
+      const float* xb = s.x(cbuf);
+      const int dc = min(a.DC, a.d - cc0);
+      const int dc4 = dc & ~3;
+#pragma unroll
+      for (int t = 0; t < kTPT; ++t) {
+        if (T[t].pt < 0) continue;
+        const float* ra[4];
+        const float* rb[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) ra[r] = xb + (T[t].row0 + T[t].rstr * r) * a.DCP;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rb[c] = xb + (T[t].col0 + T[t].cstr * c) * a.DCP;
+#pragma unroll 2
+        for (int dd = 0; dd < dc4; dd += 4) {
+          float4 va[4], vb[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) va[r] = *reinterpret_cast<const float4*>(ra[r] + dd);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) vb[c] = *reinterpret_cast<const float4*>(rb[c] + dd);
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[t][r][c] = sq_step4(acc[t][r][c], va[r], vb[c]);
+        }
+        for (int dd = dc4; dd < dc; ++dd) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[t][r][c] = sq_step(acc[t][r][c], ra[r][dd], rb[c][dd]);
+        }
+      }
+    }
+
+    // ---- offers after the last dim chunk (nndescent.cpp:160-171)
+    if (cc0 + a.DC >= a.d) {
+      u32 pass_mask[kTPT];
+      int my_q = 0;
+#pragma unroll
+      for (int t = 0; t < kTPT; ++t) {
+        pass_mask[t] = 0;
+        if (T[t].pt < 0) continue;
+        const int lb = T[t].pt * a.RMAX;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = T[t].ti + T[t].rstr * r;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int jj = T[t].tj + T[t].cstr * c;
+            bool valid;
+            int jl;
+            if (T[t].tri) {
+              valid = i < T[t].nn && jj < T[t].nn && (T[t].ti < T[t].tj || r < c);
+              jl = jj;
+            } else {
+              valid = i < T[t].nn && jj < T[t].no;
+              jl = T[t].nn + jj;
+            }
+            if (!valid) continue;
+            const float dist = __fsqrt_rn(acc[t][r][c]);
+            acc[t][r][c] = dist;
+            ++my_pairs;
+            const int bit = (r * 4 + c) * 2;
+            if (dist < s.worst(m)[lb + i]) pass_mask[t] |= 1u << bit;
+            if (dist < s.worst(m)[lb + jl]) pass_mask[t] |= 2u << bit;
+          }
+        }
+        my_q += __popc(pass_mask[t]);
+      }
+      int incl = my_q;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if ((int)lane >= o) incl += y;
+      }
+      if (lane == 31) s.misc[warp] = incl;
+      __syncthreads();
+      int wbase = 0, btot = 0;
+#pragma unroll
+      for (int w = 0; w < kJT / 32; ++w) {
+        if (w < (int)warp) wbase += s.misc[w];
+        btot += s.misc[w];
+      }
+      const u32 chunk = (u32)s.mhdr(m)[0];
+      u64* qk = a.q_key + (u64)chunk * a.q_per_chunk;
+      u32* qt = a.q_tgt + (u64)chunk * a.q_per_chunk;
+      const u32 qu = m ? q_used1 : q_used0;
+      u64 slot = qu + wbase + incl - my_q;
+      if (m) q_used1 += btot; else q_used0 += btot;
+#pragma unroll
+      for (int t = 0; t < kTPT; ++t) {
+        const u32 pm = pass_mask[t];
+        if (!pm) continue;
+        const int lb = T[t].pt * a.RMAX;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const u32 two = (pm >> ((r * 4 + c) * 2)) & 3u;
+            if (!two) continue;
+            const int i = T[t].ti + T[t].rstr * r;
+            const int jj = T[t].tj + T[t].cstr * c;
+            const u32 u = s.ids(m)[lb + i], v = s.ids(m)[lb + (T[t].tri ? jj : T[t].nn + jj)];
+            const float dist = acc[t][r][c];
+#pragma unroll
+            for (int dir = 0; dir < 2; ++dir) {
+              if (!((two >> dir) & 1u)) continue;
+              qk[slot] = pack_key(dist, dir ? u : v);
+              qt[slot] = dir ? v : u;
+              ++slot;
+            }
+          }
+        }
+      }
+      if (s.dhdr(cq)[2] >= s.mhdr(m)[1] && tid == 0) {  // chunk complete
+        a.q_fill[chunk] = qu + btot;
+        my_offers += qu + btot;
+      }
+    }
+    if (!have_next) break;
+    __syncthreads();  // everyone is done with buffer cbuf / desc slot before reuse
+    cq = nq;
+    cc0 = nc0;
+    cbuf = nbuf;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(kFull, my_pairs, o);
+  if (lane == 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntPairs), my_pairs);
+  if (tid == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntOffers), my_offers);
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntStagedRows), my_rows);
+  }
+}
+
+unsigned warp_grid(const Runner& r, u64 items) {
+  const u64 want = ceil_div<u64>(items, 8);
+  const u64 cap = (u64)r.num_sms * 16;
+  return (unsigned)std::max<u64>(1, std::min(want, cap));
+}
+
+}  // namespace
+
+JoinPlan plan_join(const Runner& r, int d, uint32_t k, uint32_t B) {
+  JoinPlan p;
+  const int max_rows = (int)(2 * B + k + B);
+  p.RMAX = (max_rows + 3) & ~3;
+  // Stage 32 dims at a time: a batch then holds ~430 rows = ~512 tiles, i.e.
+  // exactly 2 tiles per thread; the exact-order accumulators carry across
+  // the dim slices (registers), so the summation order is unchanged.
+  p.DC = d <= 32 ? ((d + 7) & ~7) : 32;
+  p.DCP = p.DC + 4;  // DC % 8 == 0 -> (DCP/4) odd: conflict-free LDS.128 across rows
+  int smem_max = 0;
+  KNNG_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, r.device));
+  // largest RB whose footprint fits (2 feature buffers + 2 row-id tables)
+  int rb = 1024;
+  while (rb > 0 && join_smem_bytes(p.RMAX, rb, p.DCP) + 1024 > (size_t)smem_max) rb -= 8;
+  require(rb >= max_rows, "nn_descent: feature rows too wide for the join's smem batches");
+  p.RB = rb;
+  p.smem = join_smem_bytes(p.RMAX, p.RB, p.DCP);
+  KNNG_CUDA(cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)p.smem));
+  int per_sm = 0;
+  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_join, kJT, p.smem));
+  p.grid = (unsigned)r.num_sms * (unsigned)std::max(per_sm, 1);
+  const uint64_t nn_max = 2ull * B, no_max = (uint64_t)k + B;
+  const uint64_t max_offers_pp = 2 * (nn_max * (nn_max - 1) / 2 + nn_max * no_max);
+  p.q_per_chunk = (uint64_t)G * max_offers_pp;
+  return p;
+}
+
+void launch_join_lists(const Runner& r, uint64_t n, uint32_t k, uint32_t B, int RMAX,
+                       const uint32_t* nf, const uint32_t* nfn, const uint32_t* of,
+                       const uint32_t* ofn, const uint32_t* nr, const uint32_t* nrn,
+                       const uint32_t* orv, const uint32_t* orn, uint32_t* L_ids,
+                       uint32_t* L_cnt) {
+  k_join_lists<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, B, RMAX, nf, nfn, of, ofn, nr, nrn,
+                                                      orv, orn, L_ids, L_cnt);
+  KNNG_LAUNCH_CHECK();
+}
+
+void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& l) {
+  JoinArgs a{};
+  a.X = l.X;
+  a.d = l.d;
+  a.L_ids = l.L_ids;
+  a.L_cnt = l.L_cnt;
+  a.RMAX = plan.RMAX;
+  a.worst = l.worst;
+  a.p_lo = l.p_lo;
+  a.p_hi = l.p_hi;
+  a.chunk_counter = l.chunk_counter;
+  a.q_key = l.q_key;
+  a.q_tgt = l.q_tgt;
+  a.q_fill = l.q_fill;
+  a.q_per_chunk = plan.q_per_chunk;
+  a.DC = plan.DC;
+  a.DCP = plan.DCP;
+  a.RB = plan.RB;
+  a.counters = l.counters;
+  k_join<<<plan.grid, kJT, plan.smem, r.stream>>>(a);
+  KNNG_LAUNCH_CHECK();
+}
+
+void launch_offer(const Runner& r, const JoinPlan& plan, const uint64_t* q_key,
+                  const uint32_t* q_tgt, const uint32_t* q_fill, uint32_t chunks,
+                  uint64_t* slots, uint32_t S, uint32_t nb, uint32_t ways, uint64_t* counters) {
+  if (!chunks) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>(chunks, (uint64_t)r.num_sms * 8);
+  k_offer<<<grid, 256, 0, r.stream>>>(q_key, q_tgt, q_fill, plan.q_per_chunk, chunks, slots, S,
+                                      nb, ways, counters);
+  KNNG_LAUNCH_CHECK();
+}
+
+}  // namespace knng_b200

@@ -18,47 +18,19 @@
 //                  order (:199-223), gross accepted count, worst refresh.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
+#include "join.hpp"
 #include "nndescent.hpp"
 
 namespace knng_b200 {
 namespace {
 
 constexpr u32 kNone = 0xffffffffu;
-constexpr u32 kWays = 4;  // candidate slots per hash bucket
 
 __device__ __forceinline__ u32 kmask_of(u32 k) { return k >= 32 ? kFull : ((1u << k) - 1u); }
-
-// Bucket of candidate v in point u's candidate buffer (kWays slots each).
-__device__ __forceinline__ u32 bucket_hash(u32 u, u32 v, u32 nb) {
-  u32 x = v * 0x9E3779B1u + u * 0x85EBCA77u;
-  x ^= x >> 15;
-  x *= 0x2C1B3C6Du;
-  x ^= x >> 12;
-  x *= 0x297A2D39u;
-  x ^= x >> 15;
-  return x % nb;
-}
-
-// Lock-free offer: the bucket keeps its kWays smallest distinct (dist,id)
-// keys in ascending order.  Each step atomicMin's the carried key into one
-// slot and carries the larger of (old, key) onward; slots only decrease, so
-// whatever the interleaving the final bucket is the W smallest distinct keys
-// offered -- the update is order-independent and the build deterministic.
-// A key that already cannot beat the bucket's last slot is dropped without
-// an atomic (it could never be among the W smallest).
-__device__ __forceinline__ void offer(u64* __restrict__ bucket, u32 ways, u64 key) {
-  const u64 tail = *reinterpret_cast<volatile u64*>(bucket + ways - 1);
-  if (key >= tail) return;
-  for (u32 w = 0; w < ways; ++w) {
-    const u64 old = atomicMin(reinterpret_cast<unsigned long long*>(bucket + w),
-                              (unsigned long long)key);
-    if (old == key) return;       // duplicate of a buffered candidate
-    key = old > key ? old : key;  // carry the larger one
-    if (key == kEmptyKey) return;
-  }
-}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -241,275 +213,6 @@ __global__ __launch_bounds__(256) void k_rev_select(u64 n, u32 B, u64 iter_seed,
       }
       if (lane == 0) outn[v] = B;
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// local_join nndescent.cpp:135-197 -- CTA per point
-// ---------------------------------------------------------------------------
-constexpr int kJoinThreads = 128;
-constexpr int kTPT = 2;  // micro-tiles per thread per pass
-
-struct JoinArgs {
-  const float* X;
-  u64 n;
-  int d;
-  u32 k;
-  u32 B;
-  const u32 *nf, *nfn, *of, *ofn, *nr, *nrn, *orv, *orn;
-  const float* worst;
-  u64* slots;
-  u32 S;     // slots per point (= nb * ways)
-  u32 nb;    // buckets per point
-  u32 ways;  // slots per bucket
-  u64* counters;
-  u64 p_lo, p_hi;      // point slice of this launch
-  u64* q_key;          // offer queue: CTA c owns [c * q_per_cta, (c+1) * q_per_cta)
-  u32* q_tgt;
-  u32* q_fill;         // entries used per CTA region
-  u64 q_per_cta;
-  int DC;    // dims per staged chunk (multiple of 8)
-  int DCP;   // smem row stride in floats (DCP/4 odd: conflict-free LDS.128)
-  int RMAX;  // smem rows (>= max list size, multiple of 4)
-};
-
-// Offers the join produced: every thread resolves one queued offer's
-// atomicMin cascade (full occupancy hides the L2 round trips the cascade
-// depends on).  Regions of CTAs that produced nothing are skipped.
-__global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
-                                               const u32* __restrict__ q_tgt,
-                                               const u32* __restrict__ q_fill, u64 q_per_cta,
-                                               u32 regions, u32 split, u64* __restrict__ slots,
-                                               u32 S, u32 nb, u32 ways) {
-  const u32 region = blockIdx.x / split, sub = blockIdx.x % split;
-  if (region >= regions) return;
-  const u32 fill = q_fill[region];
-  const u64 base = (u64)region * q_per_cta;
-  for (u32 e = sub * blockDim.x + threadIdx.x; e < fill; e += split * blockDim.x) {
-    const u64 key = q_key[base + e];
-    const u32 tgt = q_tgt[base + e];
-    offer(slots + (u64)tgt * S + (u64)bucket_hash(tgt, key_id(key), nb) * ways, ways, key);
-  }
-}
-
-// smem layout of one join CTA (dynamic):
-//   s_ids[RMAX] u32 | s_worst[RMAX] f32 | s_cand[RMAX] u32 | s_hash[256] u64 |
-//   s_int[16] | s_x[RMAX * DCP] f32 (feature tile)
-constexpr int kHashSlots = 256;
-
-__global__ __launch_bounds__(kJoinThreads, 4) void k_join(JoinArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  u32* s_ids = reinterpret_cast<u32*>(smem);
-  float* s_worst = reinterpret_cast<float*>(smem + a.RMAX * 4);
-  u32* s_cand = reinterpret_cast<u32*>(smem + a.RMAX * 8);
-  u64* s_hash = reinterpret_cast<u64*>(smem + a.RMAX * 12);
-  int* s_int = reinterpret_cast<int*>(smem + a.RMAX * 12 + kHashSlots * 8);
-  float* s_x = reinterpret_cast<float*>(smem + a.RMAX * 12 + kHashSlots * 8 + 64);
-  const int tid = threadIdx.x;
-  const unsigned lane = lane_id(), warp = tid >> 5;
-  const bool vec = (a.d & 3) == 0;
-  u64 my_pairs = 0, my_rows = 0, my_pts = 0;
-  u64* qk = a.q_key + (u64)blockIdx.x * a.q_per_cta;
-  u32* qt = a.q_tgt + (u64)blockIdx.x * a.q_per_cta;
-  u32 q_used = 0;  // uniform across the CTA
-
-  for (u64 p = a.p_lo + blockIdx.x; p < a.p_hi; p += gridDim.x) {
-    // ---- join lists (nndescent.cpp:135-153): new = nf U nr, old = (of U orv)
-    // \ new, first occurrence wins, order kept.  One candidate per thread;
-    // duplicates resolved through a smem hash of id -> smallest position.
-    const int a0 = a.nfn[p], a1 = a.nrn[p], a2 = a.ofn[p], a3 = a.orn[p];
-    const int tot = a0 + a1 + a2 + a3;
-    __syncthreads();  // previous point fully consumed
-    for (int t = tid; t < kHashSlots; t += kJoinThreads) s_hash[t] = kEmptyKey;
-    u32 c = kNone;
-    if (tid < tot) {
-      if (tid < a0) c = a.nf[p * a.B + tid];
-      else if (tid < a0 + a1) c = a.nr[p * a.B + (tid - a0)];
-      else if (tid < a0 + a1 + a2) c = a.of[p * a.k + (tid - a0 - a1)];
-      else c = a.orv[p * a.B + (tid - a0 - a1 - a2)];
-    }
-    __syncthreads();
-    u32 h = (c * 0x9E3779B1u) >> 24;  // 256 slots
-    const u64 mine = ((u64)c << 32) | (u32)tid;
-    if (tid < tot) {
-      while (true) {
-        const u64 old = atomicCAS(reinterpret_cast<unsigned long long*>(&s_hash[h]),
-                                  (unsigned long long)kEmptyKey, (unsigned long long)mine);
-        if (old == kEmptyKey || (u32)(old >> 32) == c) {
-          if (old != kEmptyKey) atomicMin(reinterpret_cast<unsigned long long*>(&s_hash[h]),
-                                          (unsigned long long)mine);
-          break;
-        }
-        h = (h + 1) & (kHashSlots - 1);
-      }
-    }
-    __syncthreads();
-    const bool keep = tid < tot && s_hash[h] == mine;
-    const unsigned kb = __ballot_sync(kFull, keep);
-    const unsigned nbm = __ballot_sync(kFull, keep && tid < a0 + a1);
-    if (lane == 0) {
-      s_int[warp] = __popc(kb);
-      s_int[8 + warp] = __popc(nbm);
-    }
-    __syncthreads();
-    int base = 0, nn = 0, na = 0;
-#pragma unroll
-    for (int w = 0; w < kJoinThreads / 32; ++w) {
-      if (w < (int)warp) base += s_int[w];
-      na += s_int[w];
-      nn += s_int[8 + w];
-    }
-    if (nn == 0 || na < 2) continue;  // uniform: no pairs at this point
-    if (keep) {
-      const int pos = base + __popc(kb & lanemask_lt());
-      s_ids[pos] = c;
-      s_worst[pos] = a.worst[c];
-    }
-    __syncthreads();
-    const int RT = (nn + 3) >> 2, CT = (na + 3) >> 2;
-    const int ntiles = RT * CT;
-    if (tid == 0) {
-      ++my_pts;
-      my_rows += (u64)na;
-    }
-    for (int pass = 0; pass < ntiles; pass += kJoinThreads * kTPT) {
-      float acc[kTPT][4][4];
-#pragma unroll
-      for (int m = 0; m < kTPT; ++m)
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) acc[m][r][cc] = 0.0f;
-      for (int c0 = 0; c0 < a.d; c0 += a.DC) {
-        const int dc = min(a.DC, a.d - c0);
-        if (c0 > 0 || pass > 0) __syncthreads();
-        if (vec) {
-          const int q = dc >> 2;
-          for (int t = tid; t < na * q; t += kJoinThreads) {
-            const int row = t / q, c4 = t - row * q;
-            cp_async16(s_x + row * a.DCP + c4 * 4, a.X + (u64)s_ids[row] * a.d + c0 + c4 * 4);
-          }
-          cp_async_wait_all();
-        } else {
-          for (int t = tid; t < na * dc; t += kJoinThreads) {
-            const int row = t / dc, cc = t - row * dc;
-            s_x[row * a.DCP + cc] = a.X[(u64)s_ids[row] * a.d + c0 + cc];
-          }
-        }
-        __syncthreads();
-        const int dc4 = dc & ~3;
-#pragma unroll
-        for (int m = 0; m < kTPT; ++m) {
-          const int t = pass + tid + m * kJoinThreads;
-          if (t >= ntiles) continue;
-          const int ti = t / CT, tj = t - ti * CT;
-          const float* ra[4];
-          const float* rb[4];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) ra[r] = s_x + (ti + RT * r) * a.DCP;
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) rb[cc] = s_x + (tj + CT * cc) * a.DCP;
-          for (int dd = 0; dd < dc4; dd += 4) {
-            float4 va[4], vb[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) va[r] = *reinterpret_cast<const float4*>(ra[r] + dd);
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) vb[cc] = *reinterpret_cast<const float4*>(rb[cc] + dd);
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-              for (int cc = 0; cc < 4; ++cc)
-                acc[m][r][cc] = sq_step4(acc[m][r][cc], va[r], vb[cc]);
-          }
-          for (int dd = dc4; dd < dc; ++dd) {
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-              for (int cc = 0; cc < 4; ++cc)
-                acc[m][r][cc] = sq_step(acc[m][r][cc], ra[r][dd], rb[cc][dd]);
-          }
-        }
-      }
-      // ---- offers (nndescent.cpp:160-171): worst filter against the staged
-      // snapshot; survivors appended to this CTA's queue region in HBM
-      u32 pass_mask[kTPT];
-      int my_q = 0;
-#pragma unroll
-      for (int m = 0; m < kTPT; ++m) {
-        pass_mask[m] = 0;
-        const int t = pass + tid + m * kJoinThreads;
-        if (t >= ntiles) continue;
-        const int ti = t / CT, tj = t - ti * CT;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int i = ti + RT * r;
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            const int j = tj + CT * cc;
-            if (i >= nn || j >= na || j <= i) continue;
-            const float dist = __fsqrt_rn(acc[m][r][cc]);
-            acc[m][r][cc] = dist;
-            ++my_pairs;
-            const int bit = (r * 4 + cc) * 2;
-            if (dist < s_worst[i]) pass_mask[m] |= 1u << bit;
-            if (dist < s_worst[j]) pass_mask[m] |= 2u << bit;
-          }
-        }
-        my_q += __popc(pass_mask[m]);
-      }
-      // block-wide exclusive prefix of the per-thread offer counts
-      int incl = my_q;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(kFull, incl, o);
-        if ((int)lane >= o) incl += y;
-      }
-      if (lane == 31) s_int[warp] = incl;
-      __syncthreads();
-      int wbase = 0, btot = 0;
-#pragma unroll
-      for (int w = 0; w < kJoinThreads / 32; ++w) {
-        if (w < (int)warp) wbase += s_int[w];
-        btot += s_int[w];
-      }
-      u64 slot = q_used + wbase + incl - my_q;
-      q_used += btot;
-#pragma unroll
-      for (int m = 0; m < kTPT; ++m) {
-        const u32 pm = pass_mask[m];
-        if (!pm) continue;
-        const int t = pass + tid + m * kJoinThreads;
-        const int ti = t / CT, tj = t - ti * CT;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            const u32 two = (pm >> ((r * 4 + cc) * 2)) & 3u;
-            if (!two) continue;
-            const u32 u = s_ids[ti + RT * r], v = s_ids[tj + CT * cc];
-            const float dist = acc[m][r][cc];
-#pragma unroll
-            for (int dir = 0; dir < 2; ++dir) {
-              if (!((two >> dir) & 1u)) continue;
-              qk[slot] = pack_key(dist, dir ? u : v);
-              qt[slot] = dir ? v : u;
-              ++slot;
-            }
-          }
-        }
-      }
-    }
-  }
-  if (tid == 0) a.q_fill[blockIdx.x] = q_used;
-  // one atomic per warp for the device counters
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(kFull, my_pairs, o);
-  if (lane == 0)
-    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntPairs), my_pairs);
-  if (tid == 0) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntOffers), (u64)q_used);
-    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntStagedRows), my_rows);
-    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + kCntJoinPoints), my_pts);
   }
 }
 
@@ -722,14 +425,7 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   const u32 S = nb * ways;
   DeviceGuard guard(r.device);
 
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evb = nullptr, eve = nullptr;
-  if (time_kernels) {
-    KNNG_CUDA(cudaEventCreate(&ev0));
-    KNNG_CUDA(cudaEventCreate(&ev1));
-    KNNG_CUDA(cudaEventCreate(&evb));
-    KNNG_CUDA(cudaEventCreate(&eve));
-    KNNG_CUDA(cudaEventRecord(evb, r.stream));
-  }
+  StageTimer tm(time_kernels, r.stream);
 
   DBuf<float> worst(r, n);
   DBuf<u64> slots(r, n * S);
@@ -744,65 +440,38 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   k_init<<<warp_grid(r, n), 256, 0, r.stream>>>(ds.x, n, ds.d, k, p.seed, keys, flags, worst.p);
   KNNG_LAUNCH_CHECK();
   ++launches;
+  tm.tick(kStInit);
 
-  // join launch shape
-  JoinArgs ja{};
-  ja.X = ds.x;
-  ja.n = n;
-  ja.d = ds.d;
-  ja.k = k;
-  ja.B = B;
-  ja.nf = s.nf.p;
-  ja.nfn = s.nfn.p;
-  ja.of = s.of.p;
-  ja.ofn = s.ofn.p;
-  ja.nr = s.nr.p;
-  ja.nrn = s.nrn.p;
-  ja.orv = s.orv.p;
-  ja.orn = s.orn.p;
-  ja.worst = worst.p;
-  ja.slots = slots.p;
-  ja.S = S;
-  ja.nb = nb;
-  ja.ways = ways;
-  ja.counters = counters.p;
-  const int max_rows = (int)(2 * B + k + B);
-  ja.RMAX = (max_rows + 3) & ~3;
-  ja.DC = ds.d <= 128 ? ((ds.d + 7) & ~7) : 128;
-  ja.DCP = ja.DC + 4;  // DC % 8 == 0 -> (DCP/4) odd
-  const size_t smem = (size_t)ja.RMAX * 12 + kHashSlots * 8 + 64 + (size_t)ja.RMAX * ja.DCP * 4;
-  KNNG_CUDA(cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-  int per_sm = 0;
-  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_join, kJoinThreads, smem));
-  if (per_sm < 1) per_sm = 1;
-  const unsigned jgrid = persistent_grid(r, per_sm, n);
-
-  // Offer queue: each join CTA owns a region sized for the worst case of its
-  // points (2 offers per pair, max pairs C(2B,2) + 2B(k+B)), so nothing can
-  // overflow; points are processed in slices to bound the queue to ~4 GB.
-  const u64 nn_max = 2ull * B, no_max = (u64)k + B;
-  const u64 max_offers_pp = 2 * (nn_max * (nn_max - 1) / 2 + nn_max * no_max);
+  // join lists (compact per point) + join launch shape
+  const JoinPlan plan = plan_join(r, ds.d, k, B);
+  DBuf<u32> L_ids(r, n * plan.RMAX), L_cnt(r, n);
+  // Offer queue: each point chunk owns a region sized for its worst case (2
+  // offers per pair, max pairs C(2B,2) + 2B(k+B)), so nothing can overflow;
+  // points are processed in slices to bound the queue to ~4 GB.
   size_t free_b = 0, total_b = 0;
   KNNG_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const u64 budget = std::min<u64>(4ull << 30, free_b / 4);
-  u64 slice = budget / (max_offers_pp * 12);
-  slice = std::max<u64>(slice / jgrid, 1) * jgrid;
-  if (slice > n) slice = n;
-  const u64 q_per_cta = ceil_div<u64>(slice, jgrid) * max_offers_pp;
-  DBuf<u64> q_key(r, q_per_cta * jgrid);
-  DBuf<u32> q_tgt(r, q_per_cta * jgrid), q_fill(r, jgrid);
-  ja.q_key = q_key.p;
-  ja.q_tgt = q_tgt.p;
-  ja.q_fill = q_fill.p;
-  ja.q_per_cta = q_per_cta;
-  constexpr u32 kOfferSplit = 8;
-  const u64 nslices = ceil_div<u64>(n, slice);
-  std::vector<cudaEvent_t> sev;
-  if (time_kernels) {
-    sev.resize(3 * nslices);
-    for (auto& e : sev) KNNG_CUDA(cudaEventCreate(&e));
+  u64 chunks_per_slice = std::max<u64>(1, budget / (plan.q_per_chunk * 12));
+  u64 slice = chunks_per_slice * kJoinChunk;
+  if (slice > n) {
+    slice = n;
+    chunks_per_slice = ceil_div<u64>(n, (u64)kJoinChunk);
   }
+  DBuf<u64> q_key(r, chunks_per_slice * plan.q_per_chunk);
+  DBuf<u32> q_tgt(r, chunks_per_slice * plan.q_per_chunk), q_fill(r, chunks_per_slice);
+  DBuf<u32> chunk_ctr(r, 1);
+  JoinLaunch jl;
+  jl.X = ds.x;
+  jl.d = ds.d;
+  jl.L_ids = L_ids.p;
+  jl.L_cnt = L_cnt.p;
+  jl.worst = worst.p;
+  jl.chunk_counter = chunk_ctr.p;
+  jl.q_key = q_key.p;
+  jl.q_tgt = q_tgt.p;
+  jl.q_fill = q_fill.p;
+  jl.counters = counters.p;
+  const u64 nslices = ceil_div<u64>(n, slice);
 
   if (st) *st = NndStats{};
   const double threshold = p.delta * (double)k * (double)n;
@@ -810,58 +479,58 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
     counters.zero();
     const u64 iter_seed = mix_seed(p.seed, 0x5a3f1e00ull + iter);
     sample_into(r, n, k, B, iter_seed, keys, flags, s, c, &launches);
+    tm.tick(kStSample);
+    launch_join_lists(r, n, k, B, plan.RMAX, s.nf.p, s.nfn.p, s.of.p, s.ofn.p, s.nr.p, s.nrn.p,
+                      s.orv.p, s.orn.p, L_ids.p, L_cnt.p);
+    ++launches;
+    tm.tick(kStLists);
     for (u64 si = 0; si < nslices; ++si) {
-      ja.p_lo = si * slice;
-      ja.p_hi = std::min<u64>(n, ja.p_lo + slice);
-      if (time_kernels) KNNG_CUDA(cudaEventRecord(sev[3 * si], r.stream));
-      k_join<<<jgrid, kJoinThreads, smem, r.stream>>>(ja);
-      KNNG_LAUNCH_CHECK();
-      if (time_kernels) KNNG_CUDA(cudaEventRecord(sev[3 * si + 1], r.stream));
-      k_offer<<<jgrid * kOfferSplit, 256, 0, r.stream>>>(q_key.p, q_tgt.p, q_fill.p, q_per_cta,
-                                                          jgrid, kOfferSplit, slots.p, S, nb,
-                                                          ways);
-      KNNG_LAUNCH_CHECK();
-      if (time_kernels) KNNG_CUDA(cudaEventRecord(sev[3 * si + 2], r.stream));
+      jl.p_lo = si * slice;
+      jl.p_hi = std::min<u64>(n, jl.p_lo + slice);
+      chunk_ctr.zero();
+      tm.tick(kStLists);
+      launch_join(r, plan, jl);
+      tm.tick(kStJoin);
+      launch_offer(r, plan, q_key.p, q_tgt.p, q_fill.p,
+                   (u32)ceil_div<u64>(jl.p_hi - jl.p_lo, (u64)kJoinChunk), slots.p, S, nb, ways,
+                   counters.p);
+      tm.tick(kStOffer);
       launches += 2;
     }
     k_apply<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst.p, slots.p,
                                                    counters.p);
     KNNG_LAUNCH_CHECK();
     launches += 1;
+    tm.tick(kStApply);
     KNNG_CUDA(cudaMemcpyAsync(hcount.p, counters.p, kNumCounters * sizeof(u64),
                               cudaMemcpyDeviceToHost, r.stream));
     r.sync();
+    tm.tick(kStSync);
     const u64 accepted = hcount.p[kCntAccepted];
+    if (std::getenv("KNNG_TRACE"))
+      std::fprintf(stderr, "[knng nnd] iter %llu pairs %llu offers %llu seen %llu accepted %llu\n",
+                   (unsigned long long)iter, (unsigned long long)hcount.p[kCntPairs],
+                   (unsigned long long)hcount.p[kCntOffers],
+                   (unsigned long long)hcount.p[kCntOfferSeen], (unsigned long long)accepted);
     if (st) {
       st->accepted_per_iter.push_back(accepted);
       st->iterations = iter + 1;
       st->pairs += hcount.p[kCntPairs];
       st->staged_rows += hcount.p[kCntStagedRows];
       st->offers += hcount.p[kCntOffers];
-      if (time_kernels) {
-        for (u64 si = 0; si < nslices; ++si) {
-          float ms = 0;
-          KNNG_CUDA(cudaEventElapsedTime(&ms, sev[3 * si], sev[3 * si + 1]));
-          st->join_ms += ms;
-          KNNG_CUDA(cudaEventElapsedTime(&ms, sev[3 * si + 1], sev[3 * si + 2]));
-          st->offer_ms += ms;
-          st->join_launches += 1;
-        }
-      }
+      st->offers_per_iter.push_back(hcount.p[kCntOffers]);
+      st->pairs_per_iter.push_back(hcount.p[kCntPairs]);
+      st->join_launches += nslices;
     }
     if ((double)accepted < threshold) break;
   }
-  if (time_kernels) {
-    KNNG_CUDA(cudaEventRecord(eve, r.stream));
-    KNNG_CUDA(cudaEventSynchronize(eve));
-    float ms = 0;
-    KNNG_CUDA(cudaEventElapsedTime(&ms, evb, eve));
-    if (st) st->total_ms = ms;
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-    cudaEventDestroy(evb);
-    cudaEventDestroy(eve);
-    for (auto& e : sev) cudaEventDestroy(e);
+  tm.tick(kStSync);
+  if (time_kernels && st) {
+    r.sync();
+    tm.accumulate(st->stage_ms, 8);
+    st->join_ms = st->stage_ms[kStJoin];
+    st->offer_ms = st->stage_ms[kStOffer];
+    st->total_ms = tm.total_ms();
   }
   if (st) st->launches = launches;
 }

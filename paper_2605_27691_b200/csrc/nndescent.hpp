@@ -26,17 +26,22 @@ struct NndParams {
 };
 
 // Device counters written by the kernels (read back once per iteration).
+enum NndStage : int { kStInit = 0, kStSample, kStLists, kStJoin, kStOffer, kStApply, kStSync };
+
 enum NndCounter : int {
   kCntAccepted = 0,    // gross successful knn_insert calls (nndescent.cpp:213)
   kCntPairs = 1,       // sigma evaluations (JoinCounts::pairs)
   kCntStagedRows = 2,  // feature rows staged into smem by the join (algorithmic bytes)
   kCntOffers = 3,      // offers passing the worst filter (atomicMin issued)
   kCntJoinPoints = 4,  // points with >= 1 pair
+  kCntOfferSeen = 5,   // queue entries walked by k_offer
   kNumCounters = 8
 };
 
 struct NndStats {
   std::vector<uint64_t> accepted_per_iter;
+  std::vector<uint64_t> offers_per_iter;
+  std::vector<uint64_t> pairs_per_iter;
   uint64_t iterations = 0;
   uint64_t pairs = 0;
   uint64_t staged_rows = 0;
@@ -46,6 +51,9 @@ struct NndStats {
   double join_ms = 0.0;
   double offer_ms = 0.0;  // k_offer (atomicMin cascades), summed
   double total_ms = 0.0;
+  // device time per stage: init, sample (fwd + transpose + reverse select),
+  // join lists, join, offer, apply, readback/host gap
+  double stage_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   uint64_t join_launches = 0;
   uint64_t launches = 0;  // all kernels launched by the build
 };

@@ -172,6 +172,45 @@ inline unsigned persistent_grid(const Runner& r, int per_sm, uint64_t work_items
   return (unsigned)g;
 }
 
+// Device-time breakdown by stage: tick(stage) records an event on the stream
+// and attributes the interval since the previous tick to `stage`.
+struct StageTimer {
+  bool on = false;
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> events;
+  std::vector<int> stage_of;
+  explicit StageTimer(bool enable, cudaStream_t s) : on(enable), stream(s) {
+    if (on) tick(-1);
+  }
+  StageTimer(const StageTimer&) = delete;
+  StageTimer& operator=(const StageTimer&) = delete;
+  ~StageTimer() {
+    for (auto e : events) cudaEventDestroy(e);
+  }
+  void tick(int stage) {
+    if (!on) return;
+    cudaEvent_t e;
+    KNNG_CUDA(cudaEventCreate(&e));
+    KNNG_CUDA(cudaEventRecord(e, stream));
+    events.push_back(e);
+    stage_of.push_back(stage);
+  }
+  // per-stage sums in ms (stream must be drained)
+  void accumulate(double* out, int nstages) const {
+    for (size_t i = 1; i < events.size(); ++i) {
+      float ms = 0;
+      KNNG_CUDA(cudaEventElapsedTime(&ms, events[i - 1], events[i]));
+      if (stage_of[i] >= 0 && stage_of[i] < nstages) out[stage_of[i]] += ms;
+    }
+  }
+  double total_ms() const {
+    if (events.size() < 2) return 0.0;
+    float ms = 0;
+    KNNG_CUDA(cudaEventElapsedTime(&ms, events.front(), events.back()));
+    return ms;
+  }
+};
+
 // Prefix sum (scan.cu): out[0..n] exclusive scan of in[0..n), out[n] = total.
 void exclusive_scan_u32(const Runner& r, const uint32_t* in, uint64_t* out, uint64_t n);
 

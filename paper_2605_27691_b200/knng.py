@@ -88,7 +88,9 @@ class _NndStats(C.Structure):
                 ("accepted_cap", C.c_uint64), ("pairs", C.c_uint64),
                 ("staged_rows", C.c_uint64), ("offers", C.c_uint64), ("join_ms", C.c_double),
                 ("total_ms", C.c_double), ("join_launches", C.c_uint64),
-                ("launches", C.c_uint64), ("offer_ms", C.c_double)]
+                ("launches", C.c_uint64), ("offer_ms", C.c_double),
+                ("stage_ms", C.c_double * 8), ("offers_per_iter", C.c_void_p),
+                ("pairs_per_iter", C.c_void_p)]
 
 
 class _SearchParams(C.Structure):
@@ -316,6 +318,9 @@ class NnDescentStats:
     join_ms: float = 0.0
     offer_ms: float = 0.0
     total_ms: float = 0.0
+    stage_ms: dict = dataclasses.field(default_factory=dict)
+    offers_per_iter: List[int] = dataclasses.field(default_factory=list)
+    pairs_per_iter: List[int] = dataclasses.field(default_factory=list)
     join_launches: int = 0
     launches: int = 0
 
@@ -557,6 +562,10 @@ def nn_descent(x, params: Optional[NnDescentParams] = None, stats: Optional[NnDe
     st = _NndStats()
     st.accepted_per_iter = acc.ctypes.data
     st.accepted_cap = len(acc)
+    off_it = np.zeros(max(p.max_iters, 1), np.uint64)
+    pair_it = np.zeros(max(p.max_iters, 1), np.uint64)
+    st.offers_per_iter = off_it.ctypes.data
+    st.pairs_per_iter = pair_it.ctypes.data
     _check(lib().knng_nn_descent(context().h, dev, C.byref(ds), C.byref(cp), C.byref(cg),
                                  C.byref(st) if stats is not None else None))
     if stats is not None:
@@ -564,6 +573,10 @@ def nn_descent(x, params: Optional[NnDescentParams] = None, stats: Optional[NnDe
         stats.accepted_per_iter = [int(v) for v in acc[:st.iterations]]
         stats.pairs, stats.staged_rows, stats.offers = st.pairs, st.staged_rows, st.offers
         stats.join_ms, stats.total_ms, stats.offer_ms = st.join_ms, st.total_ms, st.offer_ms
+        stats.offers_per_iter = [int(v) for v in off_it[:st.iterations]]
+        stats.pairs_per_iter = [int(v) for v in pair_it[:st.iterations]]
+        stats.stage_ms = dict(zip(("init", "sample", "lists", "join", "offer", "apply",
+                                   "readback"), list(st.stage_ms)[:7]))
         stats.join_launches, stats.launches = st.join_launches, st.launches
     return g
 
