@@ -253,13 +253,10 @@ knng_status knng_ctx_create(int num_devices, knng_ctx** out) {
         const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
         if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) KNNG_CUDA(e);
         cudaGetLastError();
-        cudaMemPool_t pool;
-        KNNG_CUDA(cudaDeviceGetDefaultMemPool(&pool, b));
-        cudaMemAccessDesc desc{};
-        desc.location.type = cudaMemLocationTypeDevice;
-        desc.location.id = a;
-        desc.flags = cudaMemAccessFlagsProtReadWrite;
-        KNNG_CUDA(cudaMemPoolSetAccess(pool, &desc, 1));
+        // Pool memory stays device-private: cross-GPU transfers are explicit
+        // cudaMemcpyPeerAsync pulls (ThreadWorld), which need no pool mapping,
+        // and mapping every pool allocation into all peers made pool growth
+        // fail spuriously on 2-GPU boxes.
       }
     }
     *out = ctx.release();

@@ -3,7 +3,7 @@
 // Per iteration (nndescent.cpp:247-257):
 //   k_sample_fwd   warp per point: forward new/old samples, exactly the
 //                  reference's sampling stream (nndescent.cpp:80-104)
-//   scan + k_fill_rev + k_rev_select: the serial transpose (:108-113) as a
+//   scan + k_make_pairs + radix sort + k_rev_select: the serial transpose (:108-113) as a
 //                  counting sort; each reverse list is ranked in ascending
 //                  source order and sampled with the reference's rng stream
 //                  (:114-127), so the sampled lists equal the reference's.
@@ -24,6 +24,7 @@
 
 #include "join.hpp"
 #include "nndescent.hpp"
+#include "radix.hpp"
 
 namespace knng_b200 {
 namespace {
@@ -138,28 +139,19 @@ __global__ __launch_bounds__(256) void k_sample_fwd(const u64* __restrict__ keys
   }
 }
 
-// Reverse lists: append p to the CSR segment of every forward target.
-__global__ __launch_bounds__(256) void k_fill_rev(u64 n, u32 k, u32 B, const u32* __restrict__ nf,
-                                                  const u32* __restrict__ nfn,
-                                                  const u32* __restrict__ of,
-                                                  const u32* __restrict__ ofn,
-                                                  const u64* __restrict__ off_new,
-                                                  const u64* __restrict__ off_old,
-                                                  u32* __restrict__ cur_new,
-                                                  u32* __restrict__ cur_old,
-                                                  u32* __restrict__ buf_new,
-                                                  u32* __restrict__ buf_old) {
-  const unsigned lane = lane_id();
-  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
-  for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); p < n; p += warps) {
-    if (lane < nfn[p]) {
-      const u32 id = nf[p * B + lane];
-      buf_new[off_new[id] + atomicAdd(&cur_new[id], 1u)] = (u32)p;
-    }
-    if (lane < ofn[p]) {
-      const u32 id = of[p * k + lane];
-      buf_old[off_old[id] + atomicAdd(&cur_old[id], 1u)] = (u32)p;
-    }
+// Reverse lists: (target, source) pairs in ascending source order; invalid
+// slots get key n (sorted past every real target).  A stable radix sort by
+// target then lays out every reverse list in ascending source order.
+__global__ void k_make_pairs(u64 n, u32 width, const u32* __restrict__ fwd,
+                             const u32* __restrict__ cnt, u32* __restrict__ keys,
+                             u32* __restrict__ vals) {
+  const u64 total = n * width;
+  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (u64)gridDim.x * blockDim.x) {
+    const u64 p = t / width;
+    const u32 i = (u32)(t - p * width);
+    keys[t] = i < cnt[p] ? fwd[t] : (u32)n;
+    vals[t] = (u32)p;
   }
 }
 
@@ -186,13 +178,12 @@ __global__ __launch_bounds__(256) void k_rev_select(u64 n, u32 B, u64 iter_seed,
       const u64 lo = off[v];
       const u32 len = (u32)(off[v + 1] - lo);
       const u32* seg = buf + lo;
-      if (len <= B) {
-        u64 e = lane < len ? (u64)seg[lane] : kEmptyKey;
-        e = warp_sort32(e);
-        if (lane < len) out[lane] = (u32)e;
+      if (len <= B) {  // already in ascending source order
+        if (lane < len) out[lane] = seg[lane];
         if (lane == 0) outn[v] = len;
         continue;
       }
+      // sample_distinct(len, B, rng) rng.hpp:66-87 over the sorted segment
       u32 my_pick = kNone;
       for (u32 cnt = 0; cnt < B;) {
         const u32 x = (u32)rng.next_below(len);
@@ -200,17 +191,7 @@ __global__ __launch_bounds__(256) void k_rev_select(u64 n, u32 B, u64 iter_seed,
         if (lane == cnt) my_pick = x;
         ++cnt;
       }
-      for (u32 base = 0; base < len; base += 32) {
-        const u32 idx = base + lane;
-        const u32 e = idx < len ? seg[idx] : kNone;
-        u32 rank = 0;
-        for (u32 j = 0; j < len; ++j) rank += (seg[j] < e) ? 1u : 0u;
-        if (idx >= len) rank = kNone;
-        for (u32 i = 0; i < B; ++i) {
-          const u32 pi = __shfl_sync(kFull, my_pick, i);
-          if (rank == pi) out[i] = e;
-        }
-      }
+      if (lane < B) out[lane] = seg[my_pick];
       if (lane == 0) outn[v] = B;
     }
   }
@@ -355,7 +336,7 @@ namespace {
 struct RevCsr {
   DBuf<u32> cnt_new, cnt_old;
   DBuf<u64> off_new, off_old;
-  DBuf<u32> buf_new, buf_old;
+  DBuf<u32> key_new, val_new, key_old, val_old, tk_new, tv_new, tk_old, tv_old;
 };
 
 void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_seed,
@@ -369,16 +350,18 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
   KNNG_LAUNCH_CHECK();
   exclusive_scan_u32(r, c.cnt_new.p, c.off_new.p, n);
   exclusive_scan_u32(r, c.cnt_old.p, c.off_old.p, n);
-  c.cnt_new.zero();
-  c.cnt_old.zero();
-  k_fill_rev<<<g, 256, 0, r.stream>>>(n, k, B, s.nf.p, s.nfn.p, s.of.p, s.ofn.p, c.off_new.p,
-                                      c.off_old.p, c.cnt_new.p, c.cnt_old.p, c.buf_new.p,
-                                      c.buf_old.p);
+  const unsigned eg = (unsigned)std::min<u64>(ceil_div<u64>(n * k, 256), (u64)r.num_sms * 32);
+  k_make_pairs<<<eg, 256, 0, r.stream>>>(n, B, s.nf.p, s.nfn.p, c.key_new.p, c.val_new.p);
+  k_make_pairs<<<eg, 256, 0, r.stream>>>(n, k, s.of.p, s.ofn.p, c.key_old.p, c.val_old.p);
   KNNG_LAUNCH_CHECK();
-  k_rev_select<<<g, 256, 0, r.stream>>>(n, B, iter_seed, c.off_new.p, c.buf_new.p, c.off_old.p,
-                                        c.buf_old.p, s.nr.p, s.nrn.p, s.orv.p, s.orn.p);
+  bool tn = false, to = false;
+  radix_sort_pairs(r, c.key_new.p, c.val_new.p, c.tk_new.p, c.tv_new.p, n * B, (u32)n, &tn);
+  radix_sort_pairs(r, c.key_old.p, c.val_old.p, c.tk_old.p, c.tv_old.p, n * k, (u32)n, &to);
+  k_rev_select<<<g, 256, 0, r.stream>>>(n, B, iter_seed, c.off_new.p, tn ? c.tv_new.p : c.val_new.p,
+                                        c.off_old.p, to ? c.tv_old.p : c.val_old.p, s.nr.p,
+                                        s.nrn.p, s.orv.p, s.orn.p);
   KNNG_LAUNCH_CHECK();
-  if (launches) *launches += 3 + 2 * 3;
+  if (launches) *launches += 5 + 2 * 3 + 2 * 9;
 }
 
 void alloc_lists(Runner& r, uint64_t n, uint32_t k, uint32_t B, SampleLists& s, RevCsr& c) {
@@ -396,8 +379,14 @@ void alloc_lists(Runner& r, uint64_t n, uint32_t k, uint32_t B, SampleLists& s, 
   c.cnt_old.alloc(r, n);
   c.off_new.alloc(r, n + 1);
   c.off_old.alloc(r, n + 1);
-  c.buf_new.alloc(r, n * b);
-  c.buf_old.alloc(r, n * k);
+  c.key_new.alloc(r, n * b);
+  c.val_new.alloc(r, n * b);
+  c.tk_new.alloc(r, n * b);
+  c.tv_new.alloc(r, n * b);
+  c.key_old.alloc(r, n * k);
+  c.val_old.alloc(r, n * k);
+  c.tk_old.alloc(r, n * k);
+  c.tv_old.alloc(r, n * k);
 }
 
 }  // namespace

@@ -1,0 +1,121 @@
+// radix.cu -- stable LSD radix sort of (u32 key, u32 value) pairs by key.
+//
+// Used to transpose the forward neighbor samples into reverse lists: pairs
+// (target, source) are emitted in ascending source order, so a stable sort by
+// target yields every reverse list already in ascending source order -- the
+// order of the reference's serial transpose (nndescent.cpp:108-113).
+//
+// One pass per 8-bit digit (passes = bytes of the largest key):
+//   k_radix_count   tile of 2048 items per CTA; each warp walks its 256 items
+//                   in order (8 rounds of 32) with __match_any_sync, giving
+//                   per-warp digit counts -> per-(digit, tile) totals.
+//   scan            digit-major exclusive scan -> global base of (digit, tile).
+//   k_radix_scatter same walk; the stable rank of an item is the tile base of
+//                   its digit + the counts of earlier warps + its rank within
+//                   the warp (earlier rounds, then earlier lanes).
+#include "radix.hpp"
+
+namespace knng_b200 {
+namespace {
+
+constexpr int kRT = 256;             // threads per CTA
+constexpr int kRW = kRT / 32;        // warps
+constexpr int kRItems = 8;           // rounds per warp
+constexpr int kTile = kRT * kRItems; // 2048 items per tile
+constexpr int kDigits = 256;
+
+__global__ __launch_bounds__(kRT) void k_radix_count(const u32* __restrict__ keys, u64 n,
+                                                     int shift, u32* __restrict__ hist,
+                                                     u64 ntiles) {
+  __shared__ u32 s_cnt[kRW][kDigits];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  for (int d = threadIdx.x; d < kRW * kDigits; d += kRT) (&s_cnt[0][0])[d] = 0;
+  __syncthreads();
+  const u64 t0 = (u64)blockIdx.x * kTile + (u64)warp * 32 * kRItems;
+  for (int r = 0; r < kRItems; ++r) {
+    const u64 i = t0 + (u64)r * 32 + lane;
+    const bool valid = i < n;
+    const u32 dg = valid ? (keys[i] >> shift) & 0xffu : 0xffffffffu;
+    const unsigned peers = __match_any_sync(kFull, dg);
+    if (valid && (__ffs(peers) - 1) == (int)lane) s_cnt[warp][dg] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < kDigits; d += kRT) {
+    u32 t = 0;
+    for (int w = 0; w < kRW; ++w) t += s_cnt[w][d];
+    hist[(u64)d * ntiles + blockIdx.x] = t;
+  }
+}
+
+__global__ __launch_bounds__(kRT) void k_radix_scatter(const u32* __restrict__ keys,
+                                                       const u32* __restrict__ vals, u64 n,
+                                                       int shift, const u64* __restrict__ base,
+                                                       u64 ntiles, u32* __restrict__ okeys,
+                                                       u32* __restrict__ ovals) {
+  __shared__ u32 s_cnt[kRW][kDigits];
+  __shared__ u32 s_pre[kRW][kDigits];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  for (int d = threadIdx.x; d < kRW * kDigits; d += kRT) (&s_cnt[0][0])[d] = 0;
+  __syncthreads();
+  const u64 t0 = (u64)blockIdx.x * kTile + (u64)warp * 32 * kRItems;
+  u32 dgs[kRItems], rank[kRItems];
+  for (int r = 0; r < kRItems; ++r) {
+    const u64 i = t0 + (u64)r * 32 + lane;
+    const bool valid = i < n;
+    const u32 dg = valid ? (keys[i] >> shift) & 0xffu : 0xffffffffu;
+    const unsigned peers = __match_any_sync(kFull, dg);
+    dgs[r] = dg;
+    rank[r] = 0;
+    if (valid) rank[r] = s_cnt[warp][dg] + __popc(peers & lanemask_lt());
+    __syncwarp();
+    if (valid && (__ffs(peers) - 1) == (int)lane) s_cnt[warp][dg] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // exclusive prefix over warps per digit, plus the global (digit, tile) base
+  for (int d = threadIdx.x; d < kDigits; d += kRT) {
+    u32 run = 0;
+    for (int w = 0; w < kRW; ++w) {
+      s_pre[w][d] = run;
+      run += s_cnt[w][d];
+    }
+  }
+  __syncthreads();
+  for (int r = 0; r < kRItems; ++r) {
+    const u64 i = t0 + (u64)r * 32 + lane;
+    if (i < n) {
+      const u32 dg = dgs[r];
+      const u64 pos = base[(u64)dg * ntiles + blockIdx.x] + s_pre[warp][dg] + rank[r];
+      okeys[pos] = keys[i];
+      ovals[pos] = vals[i];
+    }
+  }
+}
+
+}  // namespace
+
+void radix_sort_pairs(const Runner& r, u32* keys, u32* vals, u32* tmp_keys, u32* tmp_vals,
+                      uint64_t n, uint32_t max_key, bool* result_in_tmp) {
+  const u64 ntiles = ceil_div<u64>(n ? n : 1, (u64)kTile);
+  int passes = 0;
+  for (u64 m = max_key; m; m >>= 8) ++passes;
+  if (passes == 0) passes = 1;
+  DBuf<u32> hist(r, (u64)kDigits * ntiles);
+  DBuf<u64> base(r, (u64)kDigits * ntiles + 1);
+  u32 *ik = keys, *iv = vals, *ok = tmp_keys, *ov = tmp_vals;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = 8 * p;
+    k_radix_count<<<(unsigned)ntiles, kRT, 0, r.stream>>>(ik, n, shift, hist.p, ntiles);
+    KNNG_LAUNCH_CHECK();
+    exclusive_scan_u32(r, hist.p, base.p, (u64)kDigits * ntiles);
+    k_radix_scatter<<<(unsigned)ntiles, kRT, 0, r.stream>>>(ik, iv, n, shift, base.p, ntiles, ok,
+                                                            ov);
+    KNNG_LAUNCH_CHECK();
+    std::swap(ik, ok);
+    std::swap(iv, ov);
+  }
+  *result_in_tmp = (ik == tmp_keys);
+}
+
+}  // namespace knng_b200

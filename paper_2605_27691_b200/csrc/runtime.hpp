@@ -121,7 +121,16 @@ struct DBuf {
     n = count;
     if (count) {
       DeviceGuard g(dev);
-      KNNG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+      const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        throw CudaError(std::string("cudaMallocAsync of ") + std::to_string(count * sizeof(T)) +
+                        " bytes on device " + std::to_string(dev) + " failed: " +
+                        cudaGetErrorString(e) + " (free " + std::to_string(fr >> 20) + " MiB)");
+      }
     }
   }
   void release() noexcept {
