@@ -1,7 +1,7 @@
 /*
  * knng_c.h -- C-ABI of the B200-native kNN-graph construction path
  * (libknng_b200.so).  Drop-in boundary for the reference's public C++ API
- * (/root/reference/proj/include/knng/*.hpp): every entry point below cites the
+ * (/root/reference/proj/include/knng/ headers): every entry point below cites the
  * reference function it replaces.  Plain pointers and sizes only; no
  * exceptions cross the boundary (status codes map 1:1 onto the reference's
  * exception classes, knng_last_error() carries e.what()).

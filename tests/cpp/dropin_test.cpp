@@ -1,0 +1,154 @@
+// dropin_test.cpp -- the reference's own API, used exactly as a reference user
+// would (namespace knng, same types and calls), but compiled against
+// include/knng_b200.hpp and linked to libknng_b200.so.  Each case restates a
+// reference test (file:line in the comment); prints PASS/FAIL per case and
+// exits non-zero on any failure.
+#include <cstdio>
+#include <cstdlib>
+#include <filesystem>
+#include <functional>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "knng_b200.hpp"
+
+using namespace knng;
+
+static int g_fail = 0;
+
+static void run(const char* name, const std::function<void()>& f) {
+  try {
+    f();
+    std::printf("PASS %s\n", name);
+  } catch (const std::exception& e) {
+    ++g_fail;
+    std::printf("FAIL %s: %s\n", name, e.what());
+  }
+}
+
+static void require(bool ok, const std::string& what) {
+  if (!ok) throw std::runtime_error(what);
+}
+
+int main() {
+  run("merge_rows trivial (test_core.cpp:170-181)", [] {
+    const std::vector<NeighborEntry> a{{0, 0.1f}}, b{{1, 0.2f}};
+    auto m = merge_rows(a, b, 2);
+    require(m.size() == 2 && m[0].id == 0 && m[1].id == 1, "merge order");
+    m = merge_rows(a, a, 2);
+    require(m.size() == 1 && m[0].id == 0, "dedup");
+  });
+  run("partition offsets (test_refine.cpp:39-67)", [] {
+    const Dataset d8 = gen_random_dataset(8, 4, Distribution::uniform, 1);
+    const Partition p4 = partition_dataset(d8, 4, 5);
+    require(p4.offsets == std::vector<std::size_t>{0, 2, 4, 6, 8}, "offsets");
+    std::set<PointId> seen(p4.to_external.begin(), p4.to_external.end());
+    require(seen.size() == 8, "permutation");
+    for (std::size_t r = 0; r < 4; ++r)
+      for (std::size_t i = 0; i < p4.size_of(r); ++i) {
+        const PointId ext = p4.to_external[p4.offsets[r] + i];
+        for (std::size_t c = 0; c < 4; ++c)
+          require(p4.locals[r].f32[i * 4 + c] == d8.f32[ext * 4 + c], "local rows");
+      }
+    const Dataset dx = gen_random_dataset(10001, 2, Distribution::uniform, 2);
+    const Partition px = partition_dataset(dx, 4, 9);
+    require(px.size_of(0) == 2501 && px.size_of(3) == 2500, "ceil split");
+    bool threw = false;
+    try {
+      partition_dataset(d8, 9, 0);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    require(threw, "P > N must throw invalid_argument");
+  });
+  run("tree_schedule worked example (test_refine.cpp:69-76)", [] {
+    require(tree_schedule(8, 2, 0, 0).partners == std::vector<std::size_t>{1}, "level 0");
+    require(tree_schedule(8, 2, 0, 1).partners == std::vector<std::size_t>{2, 3}, "level 1");
+    require(tree_levels(8, 2) == 2 && tree_levels(4, 4) == 0, "levels");
+  });
+  run("nn_descent validation (test_nndescent.cpp:288-300)", [] {
+    const Dataset d = gen_random_dataset(100, 4, Distribution::uniform, 2);
+    NnDescentParams p;
+    p.k = 8;
+    p.rho = 0.0;
+    bool threw = false;
+    try {
+      nn_descent(d, p);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    require(threw, "rho=0 must throw invalid_argument");
+  });
+  run("local build quality (acceptance.cpp:52-67)", [] {
+    const Dataset d = gen_random_dataset(20000, 16, Distribution::uniform, 4242);
+    NnDescentParams p;
+    p.k = 32;
+    p.seed = 1;
+    NnDescentStats st;
+    const KnnGraph g = nn_descent(d, p, &st);
+    const GroundTruth gt = brute_force_knng(d, 32);
+    const double r = recall_at_k(g, gt, 10);
+    std::printf("  recall@10 = %.4f after %zu iterations\n", r, st.iterations);
+    require(r >= 0.95, "recall@10 < 0.95");
+  });
+  run("P=1 build_distributed == nn_descent (test_refine.cpp:349-359)", [] {
+    const Dataset d = gen_random_dataset(2000, 16, Distribution::clustered, 3, 10);
+    RefineConfig cfg;
+    cfg.ranks = 1;
+    cfg.k = 16;
+    cfg.nn.seed = 2;
+    const DistBuildResult r = build_distributed(d, cfg);
+    NnDescentParams p;
+    p.k = 16;
+    p.seed = 2;
+    const KnnGraph g = nn_descent(d, p);
+    require(r.graph.ids == g.ids && r.graph.dists == g.dists, "P=1 differs from nn_descent");
+  });
+  run("distributed P=4 quality + comm log (acceptance.cpp:72-103, 253-322)", [] {
+    const Dataset d = gen_random_dataset(8000, 16, Distribution::clustered, 7100, 16);
+    RefineConfig cfg;
+    cfg.ranks = 4;
+    cfg.groups = 2;
+    cfg.k = 32;
+    cfg.search.beam_width = 128;
+    cfg.search.num_entry_points = 96;
+    const DistBuildResult r = build_distributed(d, cfg);
+    const GroundTruth gt = brute_force_knng(d, 32);
+    const double rec = recall_at_k(r.graph, gt, 10);
+    std::printf("  P=4 recall@10 = %.4f, %zu gets, levels %zu\n", rec, r.comm_log.size(), r.levels);
+    require(rec >= 0.9, "P=4 recall too low");
+    require(r.levels == 1 && !r.comm_log.empty(), "schedule");
+  });
+  run("optimize_graph + ann_search self queries (test_annsearch.cpp:46-58)", [] {
+    const Dataset d = gen_random_dataset(10000, 16, Distribution::uniform, 1);
+    NnDescentParams p;
+    p.k = 32;
+    p.seed = 1;
+    const KnnGraph g = nn_descent(d, p);
+    const SearchGraph sg = optimize_graph(g, d, 32);
+    SearchParams sp;
+    sp.k_s = 10;
+    sp.beam_width = 64;
+    sp.seed = 5;
+    const SearchResult res = ann_search(d, sg, d, sp);
+    std::size_t hits = 0;
+    for (std::size_t q = 0; q < res.num_queries; ++q)
+      if (res.ids_row(q)[0] == q && res.dists_row(q)[0] == 0.0f) ++hits;
+    require(hits >= 0.99 * res.num_queries, "self top-1 < 99%");
+  });
+  run("graph output round trip (evalio.cpp:274-280, wire.cpp)", [] {
+    const Dataset d = gen_random_dataset(500, 8, Distribution::gaussian, 7);
+    NnDescentParams p;
+    p.k = 8;
+    const KnnGraph g = nn_descent(d, p);
+    const auto path = std::filesystem::temp_directory_path() / "knng_dropin.knng";
+    save_graph(g, path);
+    require(std::filesystem::file_size(path) == 22 + 500 * 8 * 8, "wire size");
+    const KnnGraph h = load_graph(path);
+    require(h.ids == g.ids && h.dists == g.dists, "round trip");
+    std::filesystem::remove(path);
+  });
+  std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "ALL PASS", g_fail);
+  return g_fail ? 1 : 0;
+}

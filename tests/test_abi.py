@@ -95,3 +95,14 @@ def test_compute_without_gpu_fails_loudly(knng):
     x = np.zeros((10, 4), np.float32)
     with pytest.raises(knng.KnngError):
         knng.nn_descent(x, k=3)
+
+
+def test_cpp_dropin_compiles(knng):
+    """include/knng_b200.hpp (the reference's C++ API over the C-ABI) builds
+    and links against libknng_b200.so; tests/cpp/dropin_test.cpp restates
+    reference test cases through it (run on the GPU by test_parity_gpu)."""
+    import subprocess
+    res = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")],
+                         capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    assert os.path.exists(os.path.join(ROOT, "build", "dropin_test"))

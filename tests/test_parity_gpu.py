@@ -450,3 +450,15 @@ def test_recall_parity_vs_reference(knng, name):
     gt, _ = knng.brute_force_knng(x, 10, rows=rows)
     mine = recall(ids[rows.astype(np.int64)], gt)
     assert mine >= ref["recall_at_10"] - 0.005, (mine, ref["recall_at_10"])
+
+
+def test_cpp_dropin_reference_cases(knng):
+    """The reference's C++ API (include/knng_b200.hpp) running reference test
+    cases end to end on the B200 (tests/cpp/dropin_test.cpp)."""
+    import subprocess
+    root = os.path.dirname(HERE)
+    subprocess.run(["make", "-s", "-C", os.path.join(root, "tests", "cpp")], check=True)
+    res = subprocess.run([os.path.join(root, "build", "dropin_test")], capture_output=True,
+                         text=True, timeout=600)
+    print(res.stdout)
+    assert res.returncode == 0, res.stdout + res.stderr
