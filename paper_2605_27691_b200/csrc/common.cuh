@@ -99,11 +99,25 @@ __device__ __forceinline__ float sq_step(float acc, float a, float b) {
   return __fadd_rn(acc, __fmul_rn(t, t));
 }
 
+// Two dims at once: the differences and squares use Blackwell's packed
+// FADD2/FMUL2 (IEEE round-to-nearest per component, identical to the scalar
+// ops); the accumulation stays scalar and sequential.  A packed accumulate
+// would be contracted by ptxas into FFMA2 (single rounding) -- measured to
+// change 31% of distances -- so the adds must not be f32x2.
+__device__ __forceinline__ float sq_step2(float acc, float a0, float a1, float b0, float b1) {
+  unsigned long long A, B, T;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(A) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(T) : "l"(A), "l"(B));
+  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(T) : "l"(T));
+  float s0, s1;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(s0), "=f"(s1) : "l"(T));
+  return __fadd_rn(__fadd_rn(acc, s0), s1);
+}
+
 __device__ __forceinline__ float sq_step4(float acc, float4 a, float4 b) {
-  acc = sq_step(acc, a.x, b.x);
-  acc = sq_step(acc, a.y, b.y);
-  acc = sq_step(acc, a.z, b.z);
-  return sq_step(acc, a.w, b.w);
+  acc = sq_step2(acc, a.x, a.y, b.x, b.y);
+  return sq_step2(acc, a.z, a.w, b.z, b.w);
 }
 
 // Full exact distance between two global/shared rows.

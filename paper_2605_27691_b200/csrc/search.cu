@@ -4,25 +4,56 @@
 // One warp per query (persistent CTAs of one warp).  Per query the warp keeps
 //   * the beam: a sorted array of packed (dist,id) keys in smem, double
 //     buffered, plus an "expanded" bitmask (BeamEntry, annsearch.cpp:19-31);
-//   * the visited set: an exact open-addressing hash of ids in smem (4096
-//     slots); if a query ever visits more than 3/4 of that, the set migrates
-//     to a per-warp tagged table in global memory, so membership stays exact
-//     (VisitedSet, annsearch.cpp:35-46) -- no point is ever scored twice;
-//   * the query vector in smem.
+//   * the visited set (VisitedSet, annsearch.cpp:35-46) as an open-addressing
+//     hash of ids in smem, in one of two modes:
+//       exact  -- (per-query diagnostics requested) 4096 slots; a query that
+//                 visits more than 3/4 of that migrates to a per-warp tagged
+//                 table in global memory, so no point is ever scored twice and
+//                 `scored` equals the reference's visited.size();
+//       cache  -- (no diagnostics) the entry points are drawn against an
+//                 exact set (sample_distinct needs exact distinctness); the
+//                 expansion then uses the table as a lossy 2-way direct-mapped
+//                 filter of ids (plain loads/stores, no probing).  It has no
+//                 false positives, so a fresh id is always scored.  A visited
+//                 id it forgot is either in the beam -- re-scoring gives the
+//                 identical (dist,id) key and the merge drops the duplicate --
+//                 or was rejected/evicted while the beam was full; the full
+//                 beam's tail only decreases, so its key is >= tail and it is
+//                 dropped again.  Ids, distances and hop counts stay
+//                 bit-identical; only wasted re-scores are added (counted in
+//                 `scored`).
+//   * the query vector in smem and a staging tile of 32 candidate rows.
 // A hop expands the first unexpanded beam entry, dedups its out-neighbors
-// (match.any), test-and-sets them in the visited set, scores the new ones with
-// exact-order distances (one lane per candidate), sorts the batch with a warp
-// bitonic network and merges it into the beam by rank (merge path).  A beam
-// after a batch is the top-`width` of (beam U batch), which is what the
-// reference's sequential beam_insert produces, so results are bit-identical.
+// (match.any), test-and-sets them in the visited set, stages the fresh rows
+// with coalesced cp.async (one row per warp instruction) into a padded smem
+// tile, and each lane sums its own row in the reference's sequential order
+// (bank-conflict-free: row stride/4 is odd).  The batch is sorted with a warp
+// bitonic network and merged into the beam by rank (merge path); a beam after
+// a batch is the top-`width` of (beam U batch), which is what the reference's
+// sequential beam_insert produces, so results are bit-identical.
 #include "search.hpp"
+
+#include <algorithm>
+#include <cstdlib>
 
 namespace knng_b200 {
 namespace {
 
 constexpr u32 kNoId = 0xffffffffu;
-constexpr int kVisH = 4096;            // smem visited slots
-constexpr int kVisLimit = kVisH * 3 / 4;
+constexpr u32 kExactVis = 4096;   // exact-mode smem slots (spills to global beyond 3/4)
+constexpr u32 kStageDims = 64;    // dims per staging chunk (smem per query sets occupancy)
+
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpa4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpa_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
 
 struct SearchArgs {
   const float* Q;
@@ -41,8 +72,15 @@ struct SearchArgs {
   u32* scored_out;
   u64* gtable;  // per-CTA tagged visited tables (gcap slots each), may be null
   u32 gcap;
-  u64* counters;  // [0] hops [1] scored [2] overflowed queries
+  u64* counters;  // [0] hops [1] scored [2] overflowed queries / cache resets
   u32 id_base;    // added to output ids
+  u32 vis_slots;  // smem visited slots (power of two)
+  u32 vis_limit;  // migrate (exact) / reset (cache) above this count
+  u32 cache;      // 1 = cache mode
+  u32 dch;        // dims per staging chunk
+  u32 stride;     // staging row stride in floats
+  u32 vec4;       // rows are 16-byte aligned (d % 4 == 0)
+  u32 pipe;       // double-buffered dim chunks
 };
 
 __device__ __forceinline__ u32 vis_hash(u32 id) {
@@ -55,7 +93,8 @@ __device__ __forceinline__ u32 vis_hash(u32 id) {
 
 struct Visited {
   u32* s;           // smem table
-  u64* g;           // global table of this CTA
+  u32 mask;         // slots - 1
+  u64* g;           // global table of this CTA (exact mode)
   u32 gcap;
   u32 tag;          // query tag for the global table
   bool global;
@@ -64,12 +103,12 @@ struct Visited {
   // Returns true if id was present (no insert); lane-parallel, ids distinct.
   __device__ __forceinline__ bool lookup(u32 id) const {
     if (!global) {
-      u32 h = vis_hash(id) & (kVisH - 1);
+      u32 h = vis_hash(id) & mask;
       while (true) {
         const u32 v = s[h];
         if (v == id) return true;
         if (v == kNoId) return false;
-        h = (h + 1) & (kVisH - 1);
+        h = (h + 1) & mask;
       }
     }
     u32 h = vis_hash(id) & (gcap - 1);
@@ -80,17 +119,18 @@ struct Visited {
       h = (h + 1) & (gcap - 1);
     }
   }
+  __device__ __forceinline__ bool insert_smem(u32 id) {
+    u32 h = vis_hash(id) & mask;
+    while (true) {
+      const u32 old = atomicCAS(&s[h], kNoId, id);
+      if (old == kNoId) return true;
+      if (old == id) return false;
+      h = (h + 1) & mask;
+    }
+  }
   // Test-and-set; returns true if newly inserted.
   __device__ __forceinline__ bool insert(u32 id) {
-    if (!global) {
-      u32 h = vis_hash(id) & (kVisH - 1);
-      while (true) {
-        const u32 old = atomicCAS(&s[h], kNoId, id);
-        if (old == kNoId) return true;
-        if (old == id) return false;
-        h = (h + 1) & (kVisH - 1);
-      }
-    }
+    if (!global) return insert_smem(id);
     u32 h = vis_hash(id) & (gcap - 1);
     const u64 mine = ((u64)tag << 32) | id;
     while (true) {
@@ -105,34 +145,148 @@ struct Visited {
       h = (h + 1) & (gcap - 1);
     }
   }
-  // Move the smem set into the global table (all lanes call).
+  // Exact mode: move the smem set into the global table (all lanes call).
   __device__ void migrate() {
     const unsigned lane = lane_id();
     __syncwarp();
     global = true;
-    for (int t = lane; t < kVisH; t += 32) {
+    for (u32 t = lane; t <= mask; t += 32) {
       const u32 id = s[t];
       if (id != kNoId) insert(id);
     }
     __syncwarp();
   }
+  // Cache mode after the entry points: a lossy 2-way direct-mapped filter
+  // (no false positives; the merge drops re-scored beam members as exact
+  // duplicate keys).  Returns true if id was not found (and records it).
+  __device__ __forceinline__ bool dm_test_and_set(u32 id) {
+    const u32 h = vis_hash(id);
+    const u32 p = h & mask & ~1u;
+    const uint2 v = *reinterpret_cast<const uint2*>(s + p);
+    if (v.x == id || v.y == id) return false;
+    s[p + ((h >> 20) & 1u)] = id;
+    return true;
+  }
+  // Switch the smem table from the exact entry-phase set to the filter,
+  // seeded with the beam's ids (all lanes call).
+  __device__ void to_filter(const u64* beam, u32 bs) {
+    const unsigned lane = lane_id();
+    __syncwarp();
+    for (u32 t = lane; t <= mask; t += 32) s[t] = kNoId;
+    __syncwarp();
+    for (u32 i = lane; i < bs; i += 32) dm_test_and_set(key_id(beam[i]));
+    __syncwarp();
+  }
 };
 
-// Merge the lane-held candidate keys (kEmptyKey = none) into the beam.
+// Exact-order L2 distances of the lanes' candidates (take = lane has one):
+// rows are staged chunk by chunk with coalesced cp.async, one row per warp
+// instruction, then each lane sums its row sequentially (l2_exact order).
+__device__ __forceinline__ u64 score_batch(const SearchArgs& a, const float* __restrict__ s_q,
+                                           float* __restrict__ s_stage, u64* __restrict__ s_ptr,
+                                           u32 id, bool take) {
+  const unsigned lane = lane_id();
+  __syncwarp();  // reconverge after the visited-set CAS loops
+  const unsigned fm = __ballot_sync(kFull, take);
+  if (!fm) return kEmptyKey;
+  // compact the fresh rows: staging slot = rank among the fresh lanes; row
+  // addresses go through smem (broadcast loads) rather than shuffles
+  const u32 nf = __popc(fm);
+  const u32 rank = __popc(fm & lanemask_lt());
+  if (take) s_ptr[rank] = (u64)(uintptr_t)(a.V + (u64)id * (u64)a.d);
+  __syncwarp();
+  float acc = 0.0f;
+  const u32 nch = ((u32)a.d + a.dch - 1) / a.dch;
+  const u32 buf_floats = 32 * a.stride;
+  // stage chunk ch into buffer `buf` (one commit group per chunk)
+  auto issue = [&](u32 ch, u32 buf) {
+    const u32 c0 = ch * a.dch;
+    const u32 cl = min(a.dch, (u32)a.d - c0);
+    float* stage = s_stage + buf * buf_floats;
+    if (a.vec4) {
+      // lanes-per-row = pow2 >= cl/4 (<= 32); 32/lpr rows per warp instruction
+      const u32 lpr = cl > 64 ? 32u : (cl > 32 ? 16u : (cl > 16 ? 8u : (cl > 8 ? 4u : (cl > 4 ? 2u : 1u))));
+      const u32 rpi = 32u / lpr;
+      const u32 g = lane / lpr, sub = lane % lpr;
+      const u32 sbase = (u32)__cvta_generic_to_shared(stage) + sub * 16;
+      const uintptr_t gofs = (uintptr_t)(c0 + sub * 4) * 4;
+      if (sub * 4 < cl) {
+        for (u32 k = g; k < nf; k += rpi) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + k * a.stride * 4),
+                       "l"((uintptr_t)s_ptr[k] + gofs) : "memory");
+          for (u32 t = sub * 4 + 128; t < cl; t += 128)
+            cpa16(stage + k * a.stride + t, reinterpret_cast<const float*>((uintptr_t)s_ptr[k]) + c0 + t);
+        }
+      }
+    } else {
+      for (u32 k = 0; k < nf; ++k) {
+        const float* src = reinterpret_cast<const float*>((uintptr_t)s_ptr[k]) + c0;
+        float* dst = stage + k * a.stride;
+        for (u32 t = lane; t < cl; t += 32) cpa4(dst + t, src + t);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  const u32 nbuf = a.pipe ? 2u : 1u;
+  issue(0, 0);
+  if (nbuf == 2 && nch > 1) issue(1, 1);
+  for (u32 ch = 0; ch < nch; ++ch) {
+    if (nbuf == 2 && ch + 1 < nch)
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+    const u32 c0 = ch * a.dch;
+    const u32 cl = min(a.dch, (u32)a.d - c0);
+    if (take) {
+      const float* qq = s_q + c0;
+      const float* my = s_stage + (ch % nbuf) * buf_floats + rank * a.stride;
+      if (a.vec4) {
+        for (u32 i = 0; i < cl; i += 4)
+          acc = sq_step4(acc, *reinterpret_cast<const float4*>(qq + i),
+                         *reinterpret_cast<const float4*>(my + i));
+      } else {
+        for (u32 i = 0; i < cl; ++i) acc = sq_step(acc, qq[i], my[i]);
+      }
+    }
+    __syncwarp();
+    if (ch + nbuf < nch) issue(ch + nbuf, ch % nbuf);
+  }
+  return take ? pack_key(__fsqrt_rn(acc), id) : kEmptyKey;
+}
+
+// Merge the lane-held candidate keys (kEmptyKey = none) into the beam.  A
+// candidate whose key is already in the beam (an id re-scored after it fell
+// out of the lossy visited filter: same id => same key) is dropped.
 __device__ __forceinline__ void beam_merge(u64 c, u64* __restrict__ s_beam, u32* __restrict__ s_exp,
                                            u64* __restrict__ s_cand, int& cur, u32& bs, u32 width) {
   const unsigned lane = lane_id();
   if (bs == width && c != kEmptyKey && c >= s_beam[cur * width + width - 1]) c = kEmptyKey;
   if (!__any_sync(kFull, c != kEmptyKey)) return;
   c = warp_sort32(c);
-  const u32 nc = __popc(__ballot_sync(kFull, c != kEmptyKey));
-  s_cand[lane] = c;
+  const u32 nc0 = __popc(__ballot_sync(kFull, c != kEmptyKey));
   const int nxt = cur ^ 1;
-  const u32 words = (width + 31) >> 5;
   u64* dst = s_beam + nxt * width;
   u32* dexp = s_exp + nxt * 32;
   const u64* src = s_beam + cur * width;
   const u32* sexp = s_exp + cur * 32;
+  // candidates: rank among the beam (# beam < c), duplicate test
+  u32 clo = 0;
+  bool keep = false;
+  if (lane < nc0) {
+    u32 hi = bs;
+    while (clo < hi) {
+      const u32 mid = (clo + hi) >> 1;
+      if (src[mid] < c) clo = mid + 1; else hi = mid;
+    }
+    keep = !(clo < bs && src[clo] == c);
+  }
+  const unsigned kb = __ballot_sync(kFull, keep);
+  if (!kb) return;
+  const u32 nc = __popc(kb);
+  const u32 ci = __popc(kb & lanemask_lt());
+  if (keep) s_cand[ci] = c;
+  const u32 words = (width + 31) >> 5;
   if (lane < words) dexp[lane] = 0;
   __syncwarp();
   // beam entries: new position = i + #cands < b
@@ -150,13 +304,8 @@ __device__ __forceinline__ void beam_merge(u64 c, u64* __restrict__ s_beam, u32*
     }
   }
   // candidates: new position = j + #beam < c
-  if (lane < nc) {
-    u32 lo = 0, hi = bs;
-    while (lo < hi) {
-      const u32 mid = (lo + hi) >> 1;
-      if (src[mid] < c) lo = mid + 1; else hi = mid;
-    }
-    const u32 pos = lane + lo;
+  if (keep) {
+    const u32 pos = ci + clo;
     if (pos < width) dst[pos] = c;
   }
   __syncwarp();
@@ -164,57 +313,85 @@ __device__ __forceinline__ void beam_merge(u64 c, u64* __restrict__ s_beam, u32*
   bs = min(width, bs + nc);
 }
 
-__global__ __launch_bounds__(32) void k_search(SearchArgs a) {
+struct SmemLayout {
+  size_t q, vis, beam, cand, exp, stage, ptr, total;
+};
+
+__host__ __device__ inline SmemLayout search_layout(int d, u32 width, u32 vis_slots, u32 stride) {
+  SmemLayout L{};
+  size_t off = 0;
+  L.q = off;
+  off += (((size_t)d * 4) + 15) & ~size_t(15);
+  L.stage = off;
+  off += (size_t)32 * stride * 4;
+  L.beam = off;
+  off += (size_t)2 * width * 8;
+  L.cand = off;
+  off += 32 * 8;
+  L.ptr = off;
+  off += 32 * 8;
+  L.vis = off;
+  off += (size_t)vis_slots * 4;
+  L.exp = off;
+  off += 2 * 32 * 4;
+  L.total = off;
+  return L;
+}
+
+#ifndef KNNG_SEARCH_MINB
+#define KNNG_SEARCH_MINB 1
+#endif
+__global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const unsigned lane = lane_id();
   const u32 W = a.width;
-  // layout
-  float* s_q = reinterpret_cast<float*>(smem);
-  size_t off = (((size_t)a.d * 4) + 15) & ~size_t(15);
-  u32* s_vis = reinterpret_cast<u32*>(smem + off);
-  off += (size_t)kVisH * 4;
-  u64* s_beam = reinterpret_cast<u64*>(smem + off);
-  off += (size_t)2 * W * 8;
-  u64* s_cand = reinterpret_cast<u64*>(smem + off);
-  off += 32 * 8;
-  u32* s_exp = reinterpret_cast<u32*>(smem + off);  // 2 x 32 words
+  const SmemLayout L = search_layout(a.d, W, a.vis_slots, a.stride * (a.pipe ? 2 : 1));
+  float* s_q = reinterpret_cast<float*>(smem + L.q);
+  float* s_stage = reinterpret_cast<float*>(smem + L.stage);
+  u64* s_beam = reinterpret_cast<u64*>(smem + L.beam);
+  u64* s_cand = reinterpret_cast<u64*>(smem + L.cand);
+  u64* s_ptr = reinterpret_cast<u64*>(smem + L.ptr);
+  u32* s_vis = reinterpret_cast<u32*>(smem + L.vis);
+  u32* s_exp = reinterpret_cast<u32*>(smem + L.exp);
 
   u64 tot_hops = 0, tot_scored = 0, tot_ovf = 0;
   for (u64 q = blockIdx.x; q < a.nq; q += gridDim.x) {
     // stage query, clear visited
     const float* qrow = a.Q + q * (u64)a.d;
     for (int t = lane; t < a.d; t += 32) s_q[t] = qrow[t];
-    for (int t = lane; t < kVisH; t += 32) s_vis[t] = kNoId;
+    for (u32 t = lane; t < a.vis_slots; t += 32) s_vis[t] = kNoId;
     __syncwarp();
-    Visited vis{s_vis, a.gtable ? a.gtable + (u64)blockIdx.x * a.gcap : nullptr, a.gcap,
-                (u32)(q + 1), false, 0};
+    Visited vis{s_vis, a.vis_slots - 1, a.gtable ? a.gtable + (u64)blockIdx.x * a.gcap : nullptr,
+                a.gcap, (u32)(q + 1), false, 0};
     int cur = 0;
     u32 bs = 0;
     u32 scored = 0;
 
-    auto score_and_merge = [&](u32 id, bool take) {
-      u64 c = kEmptyKey;
-      if (take) c = pack_key(l2_exact(s_q, a.V + (u64)id * a.d, a.d), id);
-      beam_merge(c, s_beam, s_exp, s_cand, cur, bs, W);
-    };
-    auto maybe_migrate = [&](u32 add) {
+    // exact mode: spill before the batch can overfill the smem table
+    auto after_insert = [&](u32 add) {
       vis.count += add;
-      if (!vis.global && vis.count > (u32)kVisLimit) {
+      if (!a.cache && !vis.global && vis.count > a.vis_limit) {
         if (vis.g == nullptr) __trap();  // host sizes gtable whenever overflow is possible
         vis.migrate();
         ++tot_ovf;
       }
     };
+    auto score_and_merge = [&](u32 id, bool take) {
+      const u64 c = score_batch(a, s_q, s_stage, s_ptr, id, take);
+      beam_merge(c, s_beam, s_exp, s_cand, cur, bs, W);
+    };
 
     // entry points: sample_distinct(n, entries, Rng(mix_seed(seed, 0xa11ce000+q)))
+    // (host sizes the cache so it never re-seeds before the entries are drawn)
     if (a.entries >= a.nv) {
       for (u64 base = 0; base < a.nv; base += 32) {
         const u64 id = base + lane;
         const bool take = id < a.nv;
         if (take) vis.insert((u32)id);
-        maybe_migrate(__popc(__ballot_sync(kFull, take)));
+        const u32 nt = __popc(__ballot_sync(kFull, take));
+        after_insert(nt);
         score_and_merge((u32)id, take);
-        scored += __popc(__ballot_sync(kFull, take));
+        scored += nt;
       }
     } else {
       const u64 s0 = mix_seed(a.seed, 0xa11ce000ull + a.qbase + q);
@@ -233,10 +410,11 @@ __global__ __launch_bounds__(32) void k_search(SearchArgs a) {
         const u32 ntake = __popc(__ballot_sync(kFull, take));
         got += ntake;
         scored += ntake;
-        maybe_migrate(ntake);
+        after_insert(ntake);
         score_and_merge(x, take);
       }
     }
+    if (a.cache) vis.to_filter(s_beam + cur * W, bs);
 
     // expansion loop (annsearch.cpp:103-120)
     u32 hops = 0;
@@ -257,13 +435,18 @@ __global__ __launch_bounds__(32) void k_search(SearchArgs a) {
       if (lane == 0) s_exp[cur * 32 + (idx >> 5)] |= 1u << (idx & 31);
       __syncwarp();
       for (u32 c0 = 0; c0 < a.deg; c0 += 32) {
-        const u32 nb = (c0 + lane < a.deg) ? a.sg[(u64)u * a.deg + c0 + lane] : kNoId;
+        const u32 nb = (c0 + lane < a.deg) ? __ldg(a.sg + (u64)u * a.deg + c0 + lane) : kNoId;
         const unsigned grp = __match_any_sync(kFull, nb);
         const bool cand = nb != kNoId && (__ffs(grp) - 1) == (int)lane;
-        const bool fresh = cand && vis.insert(nb);
+        bool fresh;
+        if (a.cache) {
+          fresh = cand && vis.dm_test_and_set(nb);
+        } else {
+          fresh = cand && vis.insert(nb);
+        }
         const u32 nf = __popc(__ballot_sync(kFull, fresh));
         scored += nf;
-        maybe_migrate(nf);
+        if (!a.cache) after_insert(nf);
         score_and_merge(nb, fresh);
       }
       ++hops;
@@ -301,12 +484,49 @@ u32 next_pow2(u64 v) {
   return (u32)p;
 }
 
+u32 env_u32(const char* name, u32 dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? (u32)strtoul(v, nullptr, 10) : dflt;
+}
+
+struct SearchShape {
+  u32 vis_slots, vis_limit, cache, dch, stride, vec4, pipe;
+  size_t smem;
+};
+
+SearchShape search_shape(int d, u32 width, u64 entries, bool exact) {
+  SearchShape s{};
+  s.vec4 = (d % 4) == 0;
+  const u32 dch = std::max<u32>(4, env_u32("KNNG_SEARCH_DCH", kStageDims) & ~3u);
+  if (s.vec4) {
+    s.dch = std::min<u32>(dch, (u32)d);
+    s.stride = ((s.dch / 4) % 2 == 0) ? s.dch + 4 : s.dch;  // stride/4 odd: conflict-free
+  } else {
+    s.dch = std::min<u32>(kStageDims, (u32)d);
+    s.stride = s.dch | 1u;  // odd stride: conflict-free scalar reads
+  }
+  // cache mode: the entry phase uses the table as an exact set (entries + one
+  // batch at <= 3/4 load), the expansion phase as a lossy 2-way filter.
+  u32 slots = env_u32("KNNG_SEARCH_VIS", 256);
+  const u64 need = entries + 32;
+  slots = std::max<u32>(std::max<u32>(next_pow2(slots), 64), next_pow2(need * 4 / 3 + 1));
+  if (exact || slots > 8192) {
+    s.cache = 0;
+    s.vis_slots = kExactVis;
+  } else {
+    s.cache = 1;
+    s.vis_slots = slots;
+  }
+  s.vis_limit = s.vis_slots * 3 / 4;
+  s.pipe = env_u32("KNNG_SEARCH_PIPE", 0) != 0 && (u32)d > s.dch;
+  s.smem = search_layout(d, width, s.vis_slots, s.stride * (s.pipe ? 2 : 1)).total;
+  return s;
+}
+
 }  // namespace
 
 size_t search_smem_bytes(int d, uint32_t width) {
-  size_t off = (((size_t)d * 4) + 15) & ~size_t(15);
-  off += (size_t)kVisH * 4 + (size_t)2 * width * 8 + 32 * 8 + 2 * 32 * 4;
-  return off;
+  return search_shape(d, width, width, true).smem;
 }
 
 void validate_search(uint64_t nq_dims, uint64_t v_dims, uint64_t sg_n, uint64_t nv,
@@ -330,11 +550,13 @@ void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint
   u64 entries = p.num_entry_points > p.k_s ? p.num_entry_points : p.k_s;
   if (entries > nv) entries = nv;
 
-  const size_t smem = search_smem_bytes(d, width);
+  // per-query diagnostics mirror the reference's exact visited-set size
+  const bool exact = scored != nullptr || getenv("KNNG_SEARCH_EXACT") != nullptr;
+  const SearchShape sh = search_shape(d, width, entries, exact);
   KNNG_CUDA(cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+                                 (int)sh.smem));
   int per_sm = 0;
-  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, 32, smem));
+  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, 32, sh.smem));
   if (per_sm < 1) per_sm = 1;
   const unsigned grid = persistent_grid(r, per_sm, nq);
 
@@ -357,11 +579,18 @@ void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint
   a.hops_out = hops;
   a.scored_out = scored;
   a.id_base = id_base;
+  a.vis_slots = sh.vis_slots;
+  a.vis_limit = sh.vis_limit;
+  a.cache = sh.cache;
+  a.dch = sh.dch;
+  a.stride = sh.stride;
+  a.vec4 = sh.vec4;
+  a.pipe = sh.pipe;
 
-  // worst-case visited count of one query: entries + hops * deg
+  // exact mode: worst-case visited count of one query = entries + hops * deg
   const u64 bound = entries + (u64)max_hops * deg + 32;
   DBuf<u64> gtab;
-  if (bound > (u64)kVisLimit) {
+  if (!sh.cache && bound > (u64)sh.vis_limit) {
     a.gcap = next_pow2(2 * bound);
     gtab.alloc(r, (u64)grid * a.gcap);
     gtab.zero();
@@ -370,7 +599,7 @@ void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint
   DBuf<u64> cnt(r, 4);
   cnt.zero();
   a.counters = cnt.p;
-  k_search<<<grid, 32, smem, r.stream>>>(a);
+  k_search<<<grid, 32, sh.smem, r.stream>>>(a);
   KNNG_LAUNCH_CHECK();
   if (counters) {
     u64 h[4];

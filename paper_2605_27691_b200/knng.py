@@ -20,7 +20,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libknng_b200.so")
+LIB_PATH = os.environ.get("KNNG_LIB") or os.path.join(_PKG, "libknng_b200.so")
 
 # ---------------------------------------------------------------------------
 # errors (status codes map 1:1 onto the reference's exceptions)
