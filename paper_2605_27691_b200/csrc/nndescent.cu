@@ -24,6 +24,8 @@
 
 #include "join.hpp"
 #include "nndescent.hpp"
+
+#include <chrono>
 #include "radix.hpp"
 
 namespace knng_b200 {
@@ -415,6 +417,7 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   DeviceGuard guard(r.device);
 
   StageTimer tm(time_kernels, r.stream);
+  const auto t_call = std::chrono::steady_clock::now();
 
   DBuf<float> worst(r, n);
   DBuf<u64> slots(r, n * S);
@@ -497,7 +500,9 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
     tm.tick(kStSync);
     const u64 accepted = hcount.p[kCntAccepted];
     if (std::getenv("KNNG_TRACE"))
-      std::fprintf(stderr, "[knng nnd] iter %llu pairs %llu offers %llu seen %llu accepted %llu\n",
+      std::fprintf(stderr, "[knng nnd] dev %d t %.1f ms iter %llu pairs %llu offers %llu seen %llu accepted %llu\n",
+                   r.device,
+                   1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_call).count(),
                    (unsigned long long)iter, (unsigned long long)hcount.p[kCntPairs],
                    (unsigned long long)hcount.p[kCntOffers],
                    (unsigned long long)hcount.p[kCntOfferSeen], (unsigned long long)accepted);
@@ -522,6 +527,8 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
     st->total_ms = tm.total_ms();
   }
   if (st) st->launches = launches;
+  if (slow_trace_on())
+    std::fprintf(stderr, "[knng slow] t %.1f dev %d nnd epilogue done\n", trace_clock_ms(), r.device);
 }
 
 void export_graph_device(const Runner& r, const uint64_t* keys, const uint32_t* flags,

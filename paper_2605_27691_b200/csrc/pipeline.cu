@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <exception>
 #include <memory>
 #include <thread>
@@ -29,6 +31,14 @@ uint64_t log2_exact(uint64_t v) {
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
       .count();
+}
+
+// KNNG_TRACE=1: per-rank phase timestamps (seconds since the call began)
+double g_trace_t0 = 0;
+void trace(size_t rank, const char* what) {
+  static const bool on = std::getenv("KNNG_TRACE") != nullptr;
+  if (on) std::fprintf(stderr, "[knng dist] rank %zu %-14s %8.1f ms\n", rank, what,
+                       1e3 * (now_s() - g_trace_t0));
 }
 
 const char* kDataset = "dataset";
@@ -232,6 +242,7 @@ void refine_rank(Shared& S, RankState& R, bool capture) {
   S.world->publish(R.rank, kGraph, R.keys.p, R.n_local * S.k * 8,
                    wire_region_size(RegionKind::knng, R.n_local, S.k), r);
   S.world->barrier(R.rank, r);
+  trace(R.rank, "published");
 
   double t = now_s();
   DBuf<float> span_x(r, R.n_local * S.d);
@@ -244,15 +255,18 @@ void refine_rank(Shared& S, RankState& R, bool capture) {
   }
   r.sync();
   R.tree_t = now_s() - t;
+  trace(R.rank, "tree");
 
   t = now_s();
   DBuf<u32> gs = grouped_merge(S, R, span_x.p, span_n);
   r.sync();
   R.merge_t = now_s() - t;
+  trace(R.rank, "merge");
 
   t = now_s();
   flat_refine(S, R);
   R.flat_t = now_s() - t;
+  trace(R.rank, "flat");
   if (capture) snapshot(R, S.k);
   r.sync();
 }
@@ -388,6 +402,7 @@ void build_distributed(const std::vector<int>& devices, const float* X, bool x_o
   Runner r0(devices[0]);
   DeviceGuard g0(r0.device);
   double t0 = now_s();
+  g_trace_t0 = t0;
   // dataset resident on device 0
   DBuf<float> xdev;
   const float* Xd = X;
@@ -430,6 +445,7 @@ void build_distributed(const std::vector<int>& devices, const float* X, bool x_o
     if (!x_on_device) xdev.release();
   }
   if (res) res->partition_s = now_s() - t0;
+  trace(0, "partitioned");
 
   auto local_build = [&](RankState& R) {
     Runner& r = *R.runner;
@@ -441,9 +457,14 @@ void build_distributed(const std::vector<int>& devices, const float* X, bool x_o
     DBuf<u32> flags(r, R.n_local);
     nn_descent_device(r, DevRows{R.local_x.p, R.n_local, d}, np, R.keys.p, flags.p, &R.nst,
                       true);
+    if (slow_trace_on())
+      std::fprintf(stderr, "[knng slow] t %.1f rank %zu nnd returned\n", trace_clock_ms(), R.rank);
     shift_ids_device(r, R.keys.p, R.n_local * S.k, (int64_t)offsets[R.rank]);
     r.sync();
+    if (slow_trace_on())
+      std::fprintf(stderr, "[knng slow] t %.1f rank %zu shifted+synced\n", trace_clock_ms(), R.rank);
     R.local_t = now_s() - t;
+    trace(R.rank, "local");
     if (cfg.capture_snapshots) snapshot(R, S.k);
   };
 
@@ -461,7 +482,9 @@ void build_distributed(const std::vector<int>& devices, const float* X, bool x_o
     });
   }
   const double te = now_s();
+  trace(0, "ranks joined");
   translate_all(r0, ranks, offsets, S.k, to_ext.p, out_ids, out_dists, out_on_device, -1);
+  trace(0, "translated");
   if (res) {
     fill_result(S, ranks, world.get(), res);
     res->etc_s = now_s() - te;

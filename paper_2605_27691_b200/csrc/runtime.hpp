@@ -4,7 +4,13 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 
+#include <mutex>
+#include <algorithm>
+#include <utility>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -45,6 +51,21 @@ struct DeviceGuard {
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
   }
 };
+
+// KNNG_TRACE_SLOW=1: host-side gaps > 30 ms between stage ticks, world ops.
+inline bool slow_trace_on() {
+  static const bool on = std::getenv("KNNG_TRACE_SLOW") != nullptr;
+  return on;
+}
+inline double trace_clock_ms() {
+  static const auto t0 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+inline int cur_device() {
+  int d = -1;
+  cudaGetDevice(&d);
+  return d;
+}
 
 // One stream on one device.  All kernels of a call run on it, all temporaries
 // are stream-ordered (cudaMallocAsync from the device pool, which we keep
@@ -154,23 +175,65 @@ struct DBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
-// Pinned host scratch.
+// Pinned host scratch from a process-wide free list.  cudaFreeHost waits on
+// every device and holds the driver while it does: a build_distributed whose
+// ranks each freed a 64-byte counter buffer at the end of NN-descent measured
+// stalls of up to 2.9 s (and the other GPUs' frees queued behind it).  Blocks
+// are never returned to the driver.
+struct PinnedPool {
+  static void* get(size_t bytes, size_t* got) {
+    PinnedPool& P = inst();
+    {
+      std::lock_guard<std::mutex> l(P.mu);
+      for (size_t i = 0; i < P.free_list.size(); ++i) {
+        if (P.free_list[i].second >= bytes) {
+          void* p = P.free_list[i].first;
+          *got = P.free_list[i].second;
+          P.free_list.erase(P.free_list.begin() + (std::ptrdiff_t)i);
+          return p;
+        }
+      }
+    }
+    const size_t cap = std::max<size_t>(bytes, 4096);
+    void* p = nullptr;
+    KNNG_CUDA(cudaMallocHost(&p, cap));
+    *got = cap;
+    return p;
+  }
+  static void put(void* p, size_t bytes) {
+    PinnedPool& P = inst();
+    std::lock_guard<std::mutex> l(P.mu);
+    P.free_list.emplace_back(p, bytes);
+  }
+
+ private:
+  static PinnedPool& inst() {
+    static PinnedPool* p = new PinnedPool();  // process lifetime
+    return *p;
+  }
+  std::mutex mu;
+  std::vector<std::pair<void*, size_t>> free_list;
+};
+
 template <class T>
 struct HBuf {
   T* p = nullptr;
   size_t n = 0;
+  size_t cap = 0;
   HBuf() = default;
   explicit HBuf(size_t count) { alloc(count); }
   HBuf(const HBuf&) = delete;
   HBuf& operator=(const HBuf&) = delete;
-  ~HBuf() {
-    if (p) cudaFreeHost(p);
+  ~HBuf() { release(); }
+  void release() {
+    if (p) PinnedPool::put(p, cap);
+    p = nullptr;
+    n = cap = 0;
   }
   void alloc(size_t count) {
-    if (p) cudaFreeHost(p);
-    p = nullptr;
+    release();
     n = count;
-    if (count) KNNG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), count * sizeof(T)));
+    if (count) p = static_cast<T*>(PinnedPool::get(count * sizeof(T), &cap));
   }
 };
 
@@ -184,6 +247,7 @@ inline unsigned persistent_grid(const Runner& r, int per_sm, uint64_t work_items
 // Device-time breakdown by stage: tick(stage) records an event on the stream
 // and attributes the interval since the previous tick to `stage`.
 struct StageTimer {
+  double last_host_ms = 0;
   bool on = false;
   cudaStream_t stream = nullptr;
   std::vector<cudaEvent_t> events;
@@ -197,6 +261,13 @@ struct StageTimer {
     for (auto e : events) cudaEventDestroy(e);
   }
   void tick(int stage) {
+    if (slow_trace_on()) {
+      const double t = trace_clock_ms();
+      if (last_host_ms > 0 && t - last_host_ms > 30.0)
+        std::fprintf(stderr, "[knng slow] t %.1f dev %d stage %d host %.1f ms\n", t,
+                     cur_device(), stage, t - last_host_ms);
+      last_host_ms = t;
+    }
     if (!on) return;
     cudaEvent_t e;
     KNNG_CUDA(cudaEventCreate(&e));

@@ -3,9 +3,83 @@
 #include "world.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
 #include <utility>
+#include <vector>
 
 namespace knng_b200 {
+
+namespace {
+
+// Region buffers outlive a ThreadWorld: cudaMalloc/cudaFree synchronise the
+// device (and, with peer access on, its peers), so a build that allocated its
+// snapshot regions afresh stalled behind the other GPUs' kernels.  Freed
+// regions park here per device and are reused by best fit.
+struct RegionCache {
+  struct Entry {
+    int dev;
+    uint64_t bytes;
+    void* p;
+  };
+  std::mutex mu;
+  std::vector<Entry> free_list;
+  static constexpr uint64_t kMaxCachedPerDev = uint64_t{24} << 30;
+
+  void* acquire(int dev, uint64_t bytes, uint64_t* got) {
+    {
+      std::lock_guard<std::mutex> l(mu);
+      size_t best = free_list.size();
+      for (size_t i = 0; i < free_list.size(); ++i) {
+        const Entry& e = free_list[i];
+        if (e.dev != dev || e.bytes < bytes || e.bytes > 2 * bytes + (64u << 20)) continue;
+        if (best == free_list.size() || e.bytes < free_list[best].bytes) best = i;
+      }
+      if (best != free_list.size()) {
+        void* p = free_list[best].p;
+        *got = free_list[best].bytes;
+        free_list.erase(free_list.begin() + (std::ptrdiff_t)best);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    KNNG_CUDA(cudaMalloc(&p, bytes));
+    *got = bytes;
+    return p;
+  }
+  void release(int dev, uint64_t bytes, void* p) {
+    std::vector<Entry> evict;
+    {
+      std::lock_guard<std::mutex> l(mu);
+      free_list.push_back({dev, bytes, p});
+      uint64_t total = 0;
+      for (const Entry& e : free_list)
+        if (e.dev == dev) total += e.bytes;
+      // over the cap: drop the oldest entries of this device
+      for (size_t i = 0; i < free_list.size() && total > kMaxCachedPerDev;) {
+        if (free_list[i].dev == dev) {
+          total -= free_list[i].bytes;
+          evict.push_back(free_list[i]);
+          free_list.erase(free_list.begin() + (std::ptrdiff_t)i);
+        } else {
+          ++i;
+        }
+      }
+    }
+    for (const Entry& e : evict) {
+      DeviceGuard g(e.dev);
+      cudaFree(e.p);
+    }
+  }
+};
+
+RegionCache& region_cache() {
+  static RegionCache* c = new RegionCache();  // process lifetime (freed by the driver at exit)
+  return *c;
+}
+
+}  // namespace
 
 uint64_t wire_region_size(RegionKind kind, uint64_t rows, uint64_t cols, bool u8_elems) {
   const uint64_t header = 4 + 1 + 8 + 8 + 1;  // wire.hpp:19
@@ -35,13 +109,7 @@ ThreadWorld::~ThreadWorld() {
 }
 
 void ThreadWorld::free_buf(Buf& b) {
-  if (b.p) {
-    int cur = 0;
-    cudaGetDevice(&cur);
-    cudaSetDevice(b.dev);
-    cudaFree(b.p);
-    cudaSetDevice(cur);
-  }
+  if (b.p) region_cache().release(b.dev, b.cap ? b.cap : b.bytes, b.p);
   b = Buf{};
 }
 
@@ -62,6 +130,7 @@ void ThreadWorld::throw_if_aborted() const {
 void ThreadWorld::publish(size_t rank, const std::string& name, const void* dev_ptr,
                           uint64_t bytes, uint64_t wire_bytes, Runner& r) {
   require(rank < num_ranks_, "RankWorld: rank out of range");
+  const double tp = trace_clock_ms();
   r.sync();  // the payload is final (this rank's kernels done) before the lock
   std::lock_guard<std::mutex> l(mu_);
   throw_if_aborted();
@@ -70,10 +139,10 @@ void ThreadWorld::publish(size_t rank, const std::string& name, const void* dev_
     throw WorldError("publish: region '" + name + "' already published by rank " +
                      std::to_string(rank) + " in epoch " + std::to_string(epoch_));
   Buf* target = s.has_current ? &s.staged : &s.current;
-  if (target->p && (target->bytes < bytes || target->dev != r.device)) free_buf(*target);
+  if (target->p && (target->cap < bytes || target->dev != r.device)) free_buf(*target);
   DeviceGuard g(r.device);
   if (!target->p && bytes) {
-    KNNG_CUDA(cudaMalloc(&target->p, bytes));
+    target->p = region_cache().acquire(r.device, bytes, &target->cap);
     target->dev = r.device;
   }
   target->bytes = bytes;
@@ -87,6 +156,9 @@ void ThreadWorld::publish(size_t rank, const std::string& name, const void* dev_
   if (s.has_current) s.has_staged = true; else s.has_current = true;
   s.published_once = true;
   s.last_epoch = epoch_;
+  if (slow_trace_on())
+    std::fprintf(stderr, "[knng slow] t %.1f rank %zu publish %s %.1f ms\n", trace_clock_ms(), rank,
+                 name.c_str(), trace_clock_ms() - tp);
 }
 
 uint64_t ThreadWorld::region_bytes(size_t target, const std::string& name) {
@@ -124,6 +196,16 @@ uint64_t ThreadWorld::get(size_t src, size_t target, const std::string& name, vo
 
 void ThreadWorld::barrier(size_t rank, Runner& r) {
   require(rank < num_ranks_, "RankWorld: rank out of range");
+  const double tb = trace_clock_ms();
+  struct Done {
+    size_t rank;
+    double tb;
+    ~Done() {
+      if (slow_trace_on())
+        std::fprintf(stderr, "[knng slow] t %.1f rank %zu barrier %.1f ms\n", trace_clock_ms(),
+                     rank, trace_clock_ms() - tb);
+    }
+  } done_trace{rank, tb};
   r.sync();  // this rank's pulls and publishes are complete
   std::unique_lock<std::mutex> l(mu_);
   throw_if_aborted();

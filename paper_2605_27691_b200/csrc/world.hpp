@@ -62,6 +62,7 @@ class ThreadWorld {
   struct Buf {
     void* p = nullptr;
     uint64_t bytes = 0;
+    uint64_t cap = 0;  // allocation size (buffers come from a reuse cache)
     uint64_t wire = 0;
     int dev = 0;
   };
