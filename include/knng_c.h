@@ -151,6 +151,10 @@ typedef struct {
 /* ---- library / context ----------------------------------------------- */
 int knng_abi_version(void);
 const char* knng_last_error(void);
+/* Number of CUDA kernels this library has launched in this process (all
+ * devices, all calls) -- launch accounting for benchmarks; no reference
+ * counterpart. */
+uint64_t knng_kernel_launches(void);
 /* num_devices <= 0: every visible device.  Enables NVLink peer access. */
 knng_status knng_ctx_create(int num_devices, knng_ctx** out);
 void knng_ctx_destroy(knng_ctx* ctx);

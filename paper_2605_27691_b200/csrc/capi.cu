@@ -228,6 +228,8 @@ extern "C" {
 
 int knng_abi_version(void) { return KNNG_ABI_VERSION; }
 
+uint64_t knng_kernel_launches(void) { return launch_counter().load(std::memory_order_relaxed); }
+
 const char* knng_last_error(void) { return g_err.c_str(); }
 
 knng_status knng_ctx_create(int num_devices, knng_ctx** out) {
@@ -318,6 +320,7 @@ knng_status knng_merge_rows(knng_ctx* ctx, int device, uint64_t rows, const uint
     copy_in(r, bdd.p, b_d, rows * nb, false);
     if (rows * na)
       k_pack<<<grid_for(r, rows * na), 256, 0, r.stream>>>(ai.p, ad.p, rows * na, ak.p);
+      KNNG_LAUNCH_CHECK();
     merge_rows_device(r, ak.p, nullptr, (u32)na, bi.p, bdd.p, (u32)nb, 0, rows, (u32)k, ok.p,
                       nullptr, oc.p);
     export_graph_device(r, ok.p, nullptr, rows, (u32)k, 0, oi.p, od.p, nullptr);

@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <stdint.h>
 
 #include <stdexcept>
@@ -40,7 +41,17 @@ struct CudaError : std::runtime_error {
                                    " at " + __FILE__ + ":" + std::to_string(__LINE__));   \
   } while (0)
 
-#define KNNG_LAUNCH_CHECK() KNNG_CUDA(cudaGetLastError())
+// Every kernel launch is followed by KNNG_LAUNCH_CHECK(), which also counts it
+// (process-wide; read through knng_kernel_launches()).
+inline std::atomic<unsigned long long>& launch_counter() {
+  static std::atomic<unsigned long long> c{0};
+  return c;
+}
+#define KNNG_LAUNCH_CHECK()                                               \
+  do {                                                                    \
+    ::knng_b200::launch_counter().fetch_add(1, std::memory_order_relaxed); \
+    KNNG_CUDA(cudaGetLastError());                                        \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // SplitMix64 (rng.hpp:12-63)

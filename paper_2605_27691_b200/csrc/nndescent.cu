@@ -354,6 +354,7 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
   exclusive_scan_u32(r, c.cnt_old.p, c.off_old.p, n);
   const unsigned eg = (unsigned)std::min<u64>(ceil_div<u64>(n * k, 256), (u64)r.num_sms * 32);
   k_make_pairs<<<eg, 256, 0, r.stream>>>(n, B, s.nf.p, s.nfn.p, c.key_new.p, c.val_new.p);
+  KNNG_LAUNCH_CHECK();
   k_make_pairs<<<eg, 256, 0, r.stream>>>(n, k, s.of.p, s.ofn.p, c.key_old.p, c.val_old.p);
   KNNG_LAUNCH_CHECK();
   bool tn = false, to = false;

@@ -243,8 +243,10 @@ void partition_device(Runner& r, uint64_t n, uint32_t ranks, uint64_t seed, uint
     cnt.zero();
     const unsigned g = elem_grid(r, pending);
     k_shuffle_reserve<<<g, 256, 0, r.stream>>>(cur, pending, jd.p, res.p, n);
+    KNNG_LAUNCH_CHECK();
     k_shuffle_commit<<<g, 256, 0, r.stream>>>(cur, pending, jd.p, res.p, to_external, nxt, cnt.p,
                                               n);
+    KNNG_LAUNCH_CHECK();
     k_shuffle_reset<<<g, 256, 0, r.stream>>>(cur, pending, jd.p, res.p, n);
     KNNG_LAUNCH_CHECK();
     KNNG_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, r.stream));

@@ -125,6 +125,7 @@ _vp = C.c_void_p
 _u64 = C.c_uint64
 _SIGS = {
     "knng_abi_version": (C.c_int, []),
+    "knng_kernel_launches": (C.c_uint64, []),
     "knng_last_error": (C.c_char_p, []),
     "knng_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "knng_ctx_destroy": (None, [_vp]),
@@ -456,6 +457,11 @@ class DistBuildResult:
 
 def abi_version() -> int:
     return lib().knng_abi_version()
+
+
+def kernel_launches() -> int:
+    """CUDA kernels launched by the library in this process so far."""
+    return int(lib().knng_kernel_launches())
 
 
 def gen_random_dataset(n: int, dims: int, dist: str = "uniform", seed: int = 0,
