@@ -168,8 +168,12 @@ def reference_recall(name):
     if os.path.exists(p):
         d = json.load(open(p)).get(name)
         if d:
-            return d["recall_at_10"], f"reference nn_descent, {d['sample_rows']} sampled rows"
-    return 0.981, "SURVEY.md §6 (reference nn_descent at 1M, 500 sampled rows)"
+            what = "nn_descent" if d["ranks"] == 1 else f"build_distributed P={d['ranks']}"
+            return d["recall_at_10"], (f"reference {what} on the same data and seeds, "
+                                       f"{d['sample_rows']} sampled rows ({name})")
+    if name.startswith("c2"):
+        return 0.981, "SURVEY.md §6 (reference nn_descent at 1M, 500 sampled rows)"
+    return None, f"reference not yet measured for {name} (tests/golden/make_reference_recall.py)"
 
 
 # ---------------------------------------------------------------------------
@@ -268,12 +272,15 @@ def main():
         workload = "C2: 1M x 128-d clustered(1000) fp32, k=32, nn_descent local build"
         ref_name = "c2_1m_clustered1000_k32"
     else:
-        # same data family and per-GPU size as N=1 (C2 shape): weak scaling
-        x_host = knng.gen_random_dataset(n, DIMS, "clustered", 42, 1000)
-        workload = (f"weak scaling of C2: {ngpu} x 1M x 128-d clustered(1000) fp32, k=32, "
+        # C4 regime (clustered(16), beam 128 / 96 entries) at the
+        # C5 width, 1M points per GPU (weak scaling).  clustered(1000) would
+        # leave the per-cluster kNN graphs disconnected, so random entry points
+        # could not reach a query's cluster in the remote graphs.
+        x_host = knng.gen_random_dataset(n, DIMS, "clustered", 42, 16)
+        workload = (f"C4-regime weak scaling: {ngpu} x 1M x 128-d clustered(16) fp32, k=32, "
                     f"build_distributed P={ngpu} M=2 (partition, local NN-descent, tree "
                     f"refine, grouped merge, flat refine; beam 128 / 96 entries)")
-        ref_name = None
+        ref_name = f"dist_p{ngpu}_{ngpu}m_clustered16_k32"
     gen_s = time.time() - t0
     pinned = torch.empty(x_host.shape, dtype=torch.float32, pin_memory=True)
     pinned.numpy()[:] = x_host
@@ -353,10 +360,7 @@ def main():
     g_ids = res.graph.ids if ngpu > 1 else res.ids
     rows = sample_rows(n)
     rec = recall10(knng, x_dev, g_ids, rows)
-    if ref_name:
-        ref_rec, ref_src = reference_recall(ref_name)
-    else:
-        ref_rec, ref_src = None, "not measured at this size (see DESIGN.md)"
+    ref_rec, ref_src = reference_recall(ref_name)
 
     line = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ngpu,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -414,6 +418,25 @@ def main():
                             "etc": res.etc_s}
         line["comm"] = {"gets": len(res.comm_log), "wire_bytes": sum(c.bytes for c in res.comm_log)}
         line["gpu_launches"] = int(launches)
+        # local-build phase efficiency (north_star: >= 85% 1->N on this phase):
+        # the same rank-0 share built alone on one GPU, in this run
+        part = knng.partition_dataset(x_dev, ngpu, cfg.seed, gather=False)
+        lo, hi = int(part.offsets[0]), int(part.offsets[1])
+        idx = torch.from_numpy(part.to_external[lo:hi].astype(np.int64)).to("cuda:0")
+        xs = x_dev.index_select(0, idx).contiguous()
+        p0 = knng.NnDescentParams(k=K, seed=1)
+        knng.nn_descent(xs, p0)
+        t1 = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            knng.nn_descent(xs, p0)
+            torch.cuda.synchronize()
+            t1.append(time.perf_counter() - t)
+        one = min(t1)
+        line["local_phase"] = {"ms": 1000 * res.local_s, "single_gpu_same_share_ms": 1000 * one,
+                               "efficiency": one / res.local_s if res.local_s else None,
+                               "note": "rank-0 partition built alone on one GPU in the same run"}
     print(json.dumps(line), flush=True)
     barrier(dist)
 
