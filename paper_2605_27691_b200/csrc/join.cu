@@ -99,6 +99,12 @@ __global__ __launch_bounds__(256) void k_join_lists(u64 n, u32 k, u32 B, int RMA
   u32* lst = s_list[w];
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
   for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + w; p < n; p += warps) {
+    // no new entry: the point has no new x new / new x old pair (:157-171);
+    // an empty descriptor keeps the join from gathering its old list at all
+    if (nfn[p] + nrn[p] == 0) {
+      if (lane == 0) L_cnt[p] = 0;
+      continue;
+    }
     int cnt = 0, nn = 0;
     for (int src = 0; src < 4; ++src) {
       const u32* base = src == 0 ? nf + p * B : src == 1 ? nr + p * B : src == 2 ? of + p * k
@@ -189,6 +195,7 @@ struct JoinArgs {
   const u32* L_cnt;
   int RMAX;
   const float* worst;
+  const u32* act;  // active point list (null: points p_lo..p_hi themselves)
   u64 p_lo, p_hi;
   u32* chunk_counter;
   u64* q_key;
@@ -217,7 +224,7 @@ struct Tile {
   bool tri;
 };
 
-// per meta slot (2): s_ids[G*RMAX] u32 | s_worst[G*RMAX] f32 | s_cnt[G] | hdr[4]
+// per meta slot (2): s_ids[G*RMAX] u32 | s_worst[G*RMAX] f32 | s_cnt[G] | s_pid[G] | hdr[4]
 // per desc slot (2): s_rb[G+1] | s_tb[G+1] | hdr[4]
 // misc[16] | x[2][(RB+4)*DCP]
 // Slots are addressed arithmetically (base + slot * stride) so nothing lands
@@ -236,8 +243,11 @@ struct Smem {
   __device__ u32* cnt(int m) const {
     return reinterpret_cast<u32*>(meta + m * meta_bytes + G * RMAX * 8);
   }
+  __device__ u32* pid(int m) const {
+    return reinterpret_cast<u32*>(meta + m * meta_bytes + G * RMAX * 8 + G * 4);
+  }
   __device__ int* mhdr(int m) const {  // [0] chunk, [1] np
-    return reinterpret_cast<int*>(meta + m * meta_bytes + G * RMAX * 8 + G * 4);
+    return reinterpret_cast<int*>(meta + m * meta_bytes + G * RMAX * 8 + G * 8);
   }
   __device__ int* rb(int q) const { return reinterpret_cast<int*>(desc + q * desc_bytes); }
   __device__ int* tb(int q) const { return rb(q) + (G + 1); }
@@ -253,7 +263,7 @@ __host__ __device__ inline size_t desc_slot_bytes(int RB) {
 __device__ __forceinline__ Smem carve(unsigned char* base, int RMAX, int RB, int DCP) {
   Smem s;
   s.RMAX = RMAX;
-  s.meta_bytes = (u32)((size_t)G * RMAX * 8 + G * 4 + 16);
+  s.meta_bytes = (u32)((size_t)G * RMAX * 8 + G * 8 + 16);
   s.desc_bytes = (u32)desc_slot_bytes(RB);
   s.meta = base;
   s.desc = base + 2 * s.meta_bytes;
@@ -266,7 +276,7 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int RMAX, int RB, int
 }
 
 __host__ __device__ inline size_t join_smem_bytes(int RMAX, int RB, int DCP) {
-  size_t off = 2 * ((size_t)G * RMAX * 8 + G * 4 + 16) + 2 * desc_slot_bytes(RB) + 128;
+  size_t off = 2 * ((size_t)G * RMAX * 8 + G * 8 + 16) + 2 * desc_slot_bytes(RB) + 128;
   off = (off + 15) & ~size_t(15);
   return off + 2 * (size_t)(RB + 4) * DCP * 4;
 }
@@ -281,11 +291,16 @@ __device__ bool load_chunk(const JoinArgs& a, const Smem& s, int m) {
   const u64 p0 = a.p_lo + (u64)chunk * G;
   if (p0 >= a.p_hi) return false;
   const int np = (a.p_hi - p0) < (u64)G ? (int)(a.p_hi - p0) : G;
-  if (tid < np) s.cnt(m)[tid] = a.L_cnt[p0 + tid];
+  if (tid < np) {
+    const u32 pt = a.act ? a.act[p0 + tid] : (u32)(p0 + tid);
+    s.pid(m)[tid] = pt;
+    s.cnt(m)[tid] = a.L_cnt[pt];
+  }
+  __syncthreads();
   for (int e = tid; e < np * a.RMAX; e += kJT) {
     const int j = e / a.RMAX, i = e - j * a.RMAX;
-    if (i < (int)(a.L_cnt[p0 + j] >> 16)) {
-      const u32 id = a.L_ids[(p0 + j) * a.RMAX + i];
+    if (i < (int)(s.cnt(m)[j] >> 16)) {
+      const u32 id = a.L_ids[(u64)s.pid(m)[j] * a.RMAX + i];
       s.ids(m)[e] = id;
       s.worst(m)[e] = a.worst[id];
     }
@@ -602,6 +617,16 @@ __global__ __launch_bounds__(kJT, 1) void k_join(JoinArgs a) {
   }
 }
 
+__global__ void k_active_flags(u64 n, const u32* __restrict__ L_cnt, u32* __restrict__ flag) {
+  for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (u64)gridDim.x * blockDim.x)
+    flag[p] = L_cnt[p] != 0;
+}
+__global__ void k_active_compact(u64 n, const u32* __restrict__ L_cnt, const u64* __restrict__ off,
+                                 u32* __restrict__ act) {
+  for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (u64)gridDim.x * blockDim.x)
+    if (L_cnt[p]) act[off[p]] = (u32)p;
+}
+
 unsigned warp_grid(const Runner& r, u64 items) {
   const u64 want = ceil_div<u64>(items, 8);
   const u64 cap = (u64)r.num_sms * 16;
@@ -648,6 +673,16 @@ void launch_join_lists(const Runner& r, uint64_t n, uint32_t k, uint32_t B, int 
   KNNG_LAUNCH_CHECK();
 }
 
+void build_active_list(const Runner& r, uint64_t n, const uint32_t* L_cnt, uint32_t* flag,
+                       uint64_t* off, uint32_t* act) {
+  const unsigned g = (unsigned)std::min<u64>(ceil_div<u64>(n ? n : 1, 256), (u64)r.num_sms * 16);
+  k_active_flags<<<g, 256, 0, r.stream>>>(n, L_cnt, flag);
+  KNNG_LAUNCH_CHECK();
+  exclusive_scan_u32(r, flag, off, n);
+  k_active_compact<<<g, 256, 0, r.stream>>>(n, L_cnt, off, act);
+  KNNG_LAUNCH_CHECK();
+}
+
 void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& l) {
   JoinArgs a{};
   a.X = l.X;
@@ -656,6 +691,7 @@ void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& l) {
   a.L_cnt = l.L_cnt;
   a.RMAX = plan.RMAX;
   a.worst = l.worst;
+  a.act = l.act;
   a.p_lo = l.p_lo;
   a.p_hi = l.p_hi;
   a.chunk_counter = l.chunk_counter;

@@ -37,6 +37,7 @@ struct JoinLaunch {
   const uint32_t* L_ids = nullptr;
   const uint32_t* L_cnt = nullptr;
   const float* worst = nullptr;
+  const uint32_t* act = nullptr;  // active point list; [p_lo, p_hi) index it (null: points)
   uint64_t p_lo = 0, p_hi = 0;
   uint32_t* chunk_counter = nullptr;  // zeroed before each launch
   uint64_t* q_key = nullptr;
@@ -46,6 +47,11 @@ struct JoinLaunch {
 };
 
 void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& a);
+
+// act[0 .. off[n]) = the points whose join descriptor is non-empty (a new
+// entry exists), ascending; flag/off are scratch (n and n + 1 entries).
+void build_active_list(const Runner& r, uint64_t n, const uint32_t* L_cnt, uint32_t* flag,
+                       uint64_t* off, uint32_t* act);
 
 // Resolve the queued offers of `chunks` chunk regions into the buckets.
 void launch_offer(const Runner& r, const JoinPlan& plan, const uint64_t* q_key,

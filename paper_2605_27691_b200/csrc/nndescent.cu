@@ -85,7 +85,7 @@ __global__ __launch_bounds__(256) void k_sample_fwd(const u64* __restrict__ keys
                                                     u32* __restrict__ nfn, u32* __restrict__ of,
                                                     u32* __restrict__ ofn,
                                                     u32* __restrict__ cnt_new,
-                                                    u32* __restrict__ cnt_old) {
+                                                    u32* __restrict__ cnt_old, bool count_old) {
   const unsigned lane = lane_id();
   const u32 km = kmask_of(k);
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
@@ -97,7 +97,7 @@ __global__ __launch_bounds__(256) void k_sample_fwd(const u64* __restrict__ keys
     const unsigned lt = lanemask_lt();
     if (lane < k && !isnew) {
       of[p * k + __popc(~fm & km & lt)] = id;
-      atomicAdd(&cnt_old[id], 1u);
+      if (count_old) atomicAdd(&cnt_old[id], 1u);
     }
     if (np <= B) {
       if (isnew) {
@@ -141,19 +141,66 @@ __global__ __launch_bounds__(256) void k_sample_fwd(const u64* __restrict__ keys
   }
 }
 
-// Reverse lists: (target, source) pairs in ascending source order; invalid
-// slots get key n (sorted past every real target).  A stable radix sort by
-// target then lays out every reverse list in ascending source order.
-__global__ void k_make_pairs(u64 n, u32 width, const u32* __restrict__ fwd,
-                             const u32* __restrict__ cnt, u32* __restrict__ keys,
-                             u32* __restrict__ vals) {
-  const u64 total = n * width;
-  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (u64)gridDim.x * blockDim.x) {
-    const u64 p = t / width;
-    const u32 i = (u32)(t - p * width);
-    keys[t] = i < cnt[p] ? fwd[t] : (u32)n;
-    vals[t] = (u32)p;
+// Reverse lists: (target, source) pairs emitted compacted in ascending
+// source order (prefix offsets per source), so a stable radix sort by target
+// lays out every reverse list in ascending source order -- the order of the
+// reference's serial transpose (nndescent.cpp:108-113).
+//
+// Inside nn_descent the old pairs are pruned to targets that have a new
+// entry (a new forward sample or a new reverse one): only those points join
+// (new x new, new x old -- nndescent.cpp:157-171), and each target's reverse
+// sample uses its own rng, so the lists of the joining points are unchanged
+// while late iterations sort a small fraction of the n*k old entries.
+__device__ __forceinline__ bool joins(u32 t, const u32* __restrict__ nfn,
+                                      const u32* __restrict__ cnt_new) {
+  return nfn[t] > 0 || cnt_new[t] > 0;
+}
+
+// warp per source: how many of its old entries survive the prune; counts
+// the surviving reverse entries per target
+__global__ __launch_bounds__(256) void k_old_count(u64 n, u32 k, const u32* __restrict__ of,
+                                                   const u32* __restrict__ ofn,
+                                                   const u32* __restrict__ nfn,
+                                                   const u32* __restrict__ cnt_new,
+                                                   u32* __restrict__ src_cnt,
+                                                   u32* __restrict__ cnt_old) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); p < n; p += warps) {
+    bool keep = false;
+    if (lane < ofn[p]) {
+      const u32 t = of[p * k + lane];
+      keep = joins(t, nfn, cnt_new);
+      if (keep) atomicAdd(&cnt_old[t], 1u);
+    }
+    const unsigned kb = __ballot_sync(kFull, keep);
+    if (lane == 0) src_cnt[p] = __popc(kb);
+  }
+}
+
+// warp per source: write its (kept) entries at src_off[p] + rank
+__global__ __launch_bounds__(256) void k_emit_pairs(u64 n, u32 width, const u32* __restrict__ fwd,
+                                                    const u32* __restrict__ cnt,
+                                                    const u64* __restrict__ src_off,
+                                                    const u32* __restrict__ nfn,
+                                                    const u32* __restrict__ cnt_new,
+                                                    u32* __restrict__ keys,
+                                                    u32* __restrict__ vals) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); p < n; p += warps) {
+    bool keep = false;
+    u32 t = 0;
+    if (lane < cnt[p]) {
+      t = fwd[p * width + lane];
+      keep = nfn == nullptr || joins(t, nfn, cnt_new);
+    }
+    const unsigned kb = __ballot_sync(kFull, keep);
+    if (keep) {
+      const u64 pos = src_off[p] + __popc(kb & lanemask_lt());
+      keys[pos] = t;
+      vals[pos] = (u32)p;
+    }
   }
 }
 
@@ -336,35 +383,51 @@ void init_random_graph_device(Runner& r, const DevRows& ds, uint32_t k, uint64_t
 namespace {
 
 struct RevCsr {
-  DBuf<u32> cnt_new, cnt_old;
-  DBuf<u64> off_new, off_old;
+  DBuf<u32> cnt_new, cnt_old, src_cnt;
+  DBuf<u64> off_new, off_old, src_off_new, src_off_old;
   DBuf<u32> key_new, val_new, key_old, val_old, tk_new, tv_new, tk_old, tv_old;
 };
 
 void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_seed,
-                 const uint64_t* keys, uint32_t* flags, SampleLists& s, RevCsr& c,
+                 const uint64_t* keys, uint32_t* flags, SampleLists& s, RevCsr& c, bool prune_old,
                  uint64_t* launches) {
   const unsigned g = warp_grid(r, n);
   c.cnt_new.zero();
   c.cnt_old.zero();
   k_sample_fwd<<<g, 256, 0, r.stream>>>(keys, flags, n, k, B, iter_seed, s.nf.p, s.nfn.p,
-                                        s.of.p, s.ofn.p, c.cnt_new.p, c.cnt_old.p);
+                                        s.of.p, s.ofn.p, c.cnt_new.p, c.cnt_old.p, !prune_old);
   KNNG_LAUNCH_CHECK();
+  if (prune_old) {
+    k_old_count<<<g, 256, 0, r.stream>>>(n, k, s.of.p, s.ofn.p, s.nfn.p, c.cnt_new.p,
+                                         c.src_cnt.p, c.cnt_old.p);
+    KNNG_LAUNCH_CHECK();
+    exclusive_scan_u32(r, c.src_cnt.p, c.src_off_old.p, n);
+  } else {
+    exclusive_scan_u32(r, s.ofn.p, c.src_off_old.p, n);
+  }
+  exclusive_scan_u32(r, s.nfn.p, c.src_off_new.p, n);
   exclusive_scan_u32(r, c.cnt_new.p, c.off_new.p, n);
   exclusive_scan_u32(r, c.cnt_old.p, c.off_old.p, n);
-  const unsigned eg = (unsigned)std::min<u64>(ceil_div<u64>(n * k, 256), (u64)r.num_sms * 32);
-  k_make_pairs<<<eg, 256, 0, r.stream>>>(n, B, s.nf.p, s.nfn.p, c.key_new.p, c.val_new.p);
+  k_emit_pairs<<<g, 256, 0, r.stream>>>(n, B, s.nf.p, s.nfn.p, c.src_off_new.p, nullptr, nullptr,
+                                        c.key_new.p, c.val_new.p);
   KNNG_LAUNCH_CHECK();
-  k_make_pairs<<<eg, 256, 0, r.stream>>>(n, k, s.of.p, s.ofn.p, c.key_old.p, c.val_old.p);
+  k_emit_pairs<<<g, 256, 0, r.stream>>>(n, k, s.of.p, s.ofn.p, c.src_off_old.p,
+                                        prune_old ? s.nfn.p : nullptr,
+                                        prune_old ? c.cnt_new.p : nullptr, c.key_old.p,
+                                        c.val_old.p);
   KNNG_LAUNCH_CHECK();
+  // sorts read their element counts (src_off[n]) on the device: no host sync
   bool tn = false, to = false;
-  radix_sort_pairs(r, c.key_new.p, c.val_new.p, c.tk_new.p, c.tv_new.p, n * B, (u32)n, &tn);
-  radix_sort_pairs(r, c.key_old.p, c.val_old.p, c.tk_old.p, c.tv_old.p, n * k, (u32)n, &to);
+  const u32 maxk = (u32)(n ? n - 1 : 0);
+  radix_sort_pairs_dev(r, c.key_new.p, c.val_new.p, c.tk_new.p, c.tv_new.p, n * B,
+                       c.src_off_new.p + n, maxk, &tn);
+  radix_sort_pairs_dev(r, c.key_old.p, c.val_old.p, c.tk_old.p, c.tv_old.p, n * k,
+                       c.src_off_old.p + n, maxk, &to);
   k_rev_select<<<g, 256, 0, r.stream>>>(n, B, iter_seed, c.off_new.p, tn ? c.tv_new.p : c.val_new.p,
                                         c.off_old.p, to ? c.tv_old.p : c.val_old.p, s.nr.p,
                                         s.nrn.p, s.orv.p, s.orn.p);
   KNNG_LAUNCH_CHECK();
-  if (launches) *launches += 5 + 2 * 3 + 2 * 9;
+  if (launches) *launches += 4 + (prune_old ? 2 : 1) + 4 * 3 + 2 * 9;
 }
 
 void alloc_lists(Runner& r, uint64_t n, uint32_t k, uint32_t B, SampleLists& s, RevCsr& c) {
@@ -382,6 +445,9 @@ void alloc_lists(Runner& r, uint64_t n, uint32_t k, uint32_t B, SampleLists& s, 
   c.cnt_old.alloc(r, n);
   c.off_new.alloc(r, n + 1);
   c.off_old.alloc(r, n + 1);
+  c.src_cnt.alloc(r, n);
+  c.src_off_new.alloc(r, n + 1);
+  c.src_off_old.alloc(r, n + 1);
   c.key_new.alloc(r, n * b);
   c.val_new.alloc(r, n * b);
   c.tk_new.alloc(r, n * b);
@@ -402,7 +468,8 @@ void sample_neighbors_device(Runner& r, uint64_t n, uint32_t k, double rho, uint
   const uint32_t B = bound_of(rho, k);
   RevCsr c;
   alloc_lists(r, n, k, B, out, c);
-  sample_into(r, n, k, B, mix_seed(seed, 0x5a3f1e00ull + iter), keys, flags, out, c, nullptr);
+  sample_into(r, n, k, B, mix_seed(seed, 0x5a3f1e00ull + iter), keys, flags, out, c, false,
+              nullptr);
 }
 
 void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_t* keys,
@@ -453,7 +520,11 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   DBuf<u64> q_key(r, chunks_per_slice * plan.q_per_chunk);
   DBuf<u32> q_tgt(r, chunks_per_slice * plan.q_per_chunk), q_fill(r, chunks_per_slice);
   DBuf<u32> chunk_ctr(r, 1);
+  // points with a new entry, compacted: late iterations join a small fraction
+  DBuf<u32> act(r, n), act_flag(r, n);
+  DBuf<u64> act_off(r, n + 1);
   JoinLaunch jl;
+  jl.act = act.p;
   jl.X = ds.x;
   jl.d = ds.d;
   jl.L_ids = L_ids.p;
@@ -464,22 +535,28 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   jl.q_tgt = q_tgt.p;
   jl.q_fill = q_fill.p;
   jl.counters = counters.p;
-  const u64 nslices = ceil_div<u64>(n, slice);
 
   if (st) *st = NndStats{};
   const double threshold = p.delta * (double)k * (double)n;
   for (u64 iter = 0; iter < p.max_iters; ++iter) {
     counters.zero();
     const u64 iter_seed = mix_seed(p.seed, 0x5a3f1e00ull + iter);
-    sample_into(r, n, k, B, iter_seed, keys, flags, s, c, &launches);
+    sample_into(r, n, k, B, iter_seed, keys, flags, s, c, true, &launches);
     tm.tick(kStSample);
     launch_join_lists(r, n, k, B, plan.RMAX, s.nf.p, s.nfn.p, s.of.p, s.ofn.p, s.nr.p, s.nrn.p,
                       s.orv.p, s.orn.p, L_ids.p, L_cnt.p);
     ++launches;
     tm.tick(kStLists);
+    build_active_list(r, n, L_cnt.p, act_flag.p, act_off.p, act.p);
+    launches += 5;
+    KNNG_CUDA(cudaMemcpyAsync(hcount.p + kCntActive, act_off.p + n, sizeof(u64),
+                              cudaMemcpyDeviceToHost, r.stream));
+    r.sync();
+    const u64 n_act = hcount.p[kCntActive];
+    const u64 nslices = ceil_div<u64>(n_act, slice);
     for (u64 si = 0; si < nslices; ++si) {
       jl.p_lo = si * slice;
-      jl.p_hi = std::min<u64>(n, jl.p_lo + slice);
+      jl.p_hi = std::min<u64>(n_act, jl.p_lo + slice);
       chunk_ctr.zero();
       tm.tick(kStLists);
       launch_join(r, plan, jl);

@@ -35,6 +35,7 @@ enum NndCounter : int {
   kCntOffers = 3,      // offers passing the worst filter (atomicMin issued)
   kCntJoinPoints = 4,  // points with >= 1 pair
   kCntOfferSeen = 5,   // queue entries walked by k_offer
+  kCntActive = 6,      // host scratch: points with a new entry this iteration
   kNumCounters = 8
 };
 

@@ -24,11 +24,23 @@ constexpr int kRItems = 8;           // rounds per warp
 constexpr int kTile = kRT * kRItems; // 2048 items per tile
 constexpr int kDigits = 256;
 
-__global__ __launch_bounds__(kRT) void k_radix_count(const u32* __restrict__ keys, u64 n,
-                                                     int shift, u32* __restrict__ hist,
-                                                     u64 ntiles) {
+// n_dev (optional): the live element count, read on the device (<= n)
+__device__ __forceinline__ u64 live_count(u64 n, const u64* n_dev) {
+  if (n_dev == nullptr) return n;
+  const u64 m = *n_dev;
+  return m < n ? m : n;
+}
+
+__global__ __launch_bounds__(kRT) void k_radix_count(const u32* __restrict__ keys, u64 n_cap,
+                                                     const u64* __restrict__ n_dev, int shift,
+                                                     u32* __restrict__ hist, u64 ntiles) {
   __shared__ u32 s_cnt[kRW][kDigits];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const u64 n = live_count(n_cap, n_dev);
+  if ((u64)blockIdx.x * kTile >= n) {  // empty tile: zero column
+    for (int d = threadIdx.x; d < kDigits; d += kRT) hist[(u64)d * ntiles + blockIdx.x] = 0;
+    return;
+  }
   for (int d = threadIdx.x; d < kRW * kDigits; d += kRT) (&s_cnt[0][0])[d] = 0;
   __syncthreads();
   const u64 t0 = (u64)blockIdx.x * kTile + (u64)warp * 32 * kRItems;
@@ -49,13 +61,16 @@ __global__ __launch_bounds__(kRT) void k_radix_count(const u32* __restrict__ key
 }
 
 __global__ __launch_bounds__(kRT) void k_radix_scatter(const u32* __restrict__ keys,
-                                                       const u32* __restrict__ vals, u64 n,
-                                                       int shift, const u64* __restrict__ base,
+                                                       const u32* __restrict__ vals, u64 n_cap,
+                                                       const u64* __restrict__ n_dev, int shift,
+                                                       const u64* __restrict__ base,
                                                        u64 ntiles, u32* __restrict__ okeys,
                                                        u32* __restrict__ ovals) {
   __shared__ u32 s_cnt[kRW][kDigits];
   __shared__ u32 s_pre[kRW][kDigits];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const u64 n = live_count(n_cap, n_dev);
+  if ((u64)blockIdx.x * kTile >= n) return;
   for (int d = threadIdx.x; d < kRW * kDigits; d += kRT) (&s_cnt[0][0])[d] = 0;
   __syncthreads();
   const u64 t0 = (u64)blockIdx.x * kTile + (u64)warp * 32 * kRItems;
@@ -95,8 +110,10 @@ __global__ __launch_bounds__(kRT) void k_radix_scatter(const u32* __restrict__ k
 
 }  // namespace
 
-void radix_sort_pairs(const Runner& r, u32* keys, u32* vals, u32* tmp_keys, u32* tmp_vals,
-                      uint64_t n, uint32_t max_key, bool* result_in_tmp) {
+namespace {
+
+void sort_impl(const Runner& r, u32* keys, u32* vals, u32* tmp_keys, u32* tmp_vals, u64 n,
+               const u64* n_dev, u32 max_key, bool* result_in_tmp) {
   const u64 ntiles = ceil_div<u64>(n ? n : 1, (u64)kTile);
   int passes = 0;
   for (u64 m = max_key; m; m >>= 8) ++passes;
@@ -106,16 +123,29 @@ void radix_sort_pairs(const Runner& r, u32* keys, u32* vals, u32* tmp_keys, u32*
   u32 *ik = keys, *iv = vals, *ok = tmp_keys, *ov = tmp_vals;
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
-    k_radix_count<<<(unsigned)ntiles, kRT, 0, r.stream>>>(ik, n, shift, hist.p, ntiles);
+    k_radix_count<<<(unsigned)ntiles, kRT, 0, r.stream>>>(ik, n, n_dev, shift, hist.p, ntiles);
     KNNG_LAUNCH_CHECK();
     exclusive_scan_u32(r, hist.p, base.p, (u64)kDigits * ntiles);
-    k_radix_scatter<<<(unsigned)ntiles, kRT, 0, r.stream>>>(ik, iv, n, shift, base.p, ntiles, ok,
-                                                            ov);
+    k_radix_scatter<<<(unsigned)ntiles, kRT, 0, r.stream>>>(ik, iv, n, n_dev, shift, base.p,
+                                                            ntiles, ok, ov);
     KNNG_LAUNCH_CHECK();
     std::swap(ik, ok);
     std::swap(iv, ov);
   }
   *result_in_tmp = (ik == tmp_keys);
+}
+
+}  // namespace
+
+void radix_sort_pairs(const Runner& r, u32* keys, u32* vals, u32* tmp_keys, u32* tmp_vals,
+                      uint64_t n, uint32_t max_key, bool* result_in_tmp) {
+  sort_impl(r, keys, vals, tmp_keys, tmp_vals, n, nullptr, max_key, result_in_tmp);
+}
+
+void radix_sort_pairs_dev(const Runner& r, u32* keys, u32* vals, u32* tmp_keys, u32* tmp_vals,
+                          uint64_t capacity, const uint64_t* n_dev, uint32_t max_key,
+                          bool* result_in_tmp) {
+  sort_impl(r, keys, vals, tmp_keys, tmp_vals, capacity, n_dev, max_key, result_in_tmp);
 }
 
 }  // namespace knng_b200
