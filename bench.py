@@ -243,6 +243,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ramp", action="store_true", help="skip the clock ramp (profiling runs)")
     ap.add_argument("--per-gpu", type=int, default=PER_GPU)
     args = ap.parse_args()
     ws, rank = dist_env()
@@ -304,7 +305,7 @@ def main():
     # stepping until two consecutive steps agree within 5% (cap 12 steps / 60 s)
     ramp = []
     t_ramp = time.time()
-    while len(ramp) < 12 and time.time() - t_ramp < 60:
+    while not args.no_ramp and len(ramp) < 12 and time.time() - t_ramp < 60:
         torch.cuda.synchronize()
         t = time.perf_counter()
         step(x_dev)
@@ -386,9 +387,24 @@ def main():
         per_launch = join_bytes / max(1, st.join_launches)
         avg_ms = st.join_ms / max(1, st.join_launches)
         achieved = per_launch / (avg_ms / 1000.0) / 1e9
+        traffic, traffic_src = None, None
+        tp = os.path.join(ROOT, "profiles", "r01_join_traffic.json")
+        if os.path.exists(tp):
+            tj = json.load(open(tp))
+            traffic, traffic_src = tj["traffic_bytes"], tj["capture"]
+        # the join is bound by exact-order fp32 arithmetic (sub, mul, add per
+        # dim, no FMA -- parity forbids reassociation/contraction), not HBM:
+        # report that roofline too (non-FMA fp32 peak = SMs x 128 x clock)
+        join_ops = st.pairs * DIMS * 3
+        fp32_peak = 148 * 128 * clocks.summary().get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         line["roofline"] = {"kernel": "k_join (nndescent.cu)", "bound": "hbm",
                             "achieved": achieved, "peak": peak, "unit": "GB/s",
-                            "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                            "frac": achieved / peak, "traffic": traffic,
+                            "traffic_source": traffic_src, "peak_source": peak_src,
+                            "compute": {"bound": "fp32 non-FMA (exact-order distances)",
+                                        "achieved_tops": join_ops / (st.join_ms / 1000.0) / 1e12,
+                                        "peak_tops": fp32_peak,
+                                        "frac": join_ops / (st.join_ms / 1000.0) / 1e12 / fp32_peak},
                             "algorithmic_bytes_per_launch": per_launch,
                             "avg_launch_ms": avg_ms, "join_share_of_step": st.join_ms / ms,
                             "offer_kernel_ms_per_step": st.offer_ms,
