@@ -250,13 +250,8 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args, ws, rank)
     dist = init_pg(ws)
-    if rank != 0:
-        # rank 0 drives every GPU of the build (one host thread per GPU-rank)
-        barrier(dist)
-        max_over_ranks(dist, 0.0)
-        max_over_ranks(dist, 0.0)
-        barrier(dist)
-        return
+    if ws > 1:
+        return run_multi(args, ws, rank, dist)
     import torch
 
     import paper_2605_27691_b200 as knng
@@ -454,6 +449,167 @@ def main():
                                "efficiency": one / res.local_s if res.local_s else None,
                                "note": "rank-0 partition built alone on one GPU in the same run"}
     print(json.dumps(line), flush=True)
+    barrier(dist)
+
+
+def allreduce(dist, vals, op="max"):
+    import torch
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+def run_multi(args, ws, rank, dist):
+    """N > 1 under torchrun: one process per GPU.  Every rank builds and
+    refines its own share on its own GPU (knng_build_distributed_rank; CUDA
+    IPC handles over the gloo group, one-sided NVLink pulls); each rank times
+    its steps with CUDA events on its own stream, the max over ranks is the
+    step time."""
+    import torch
+
+    import paper_2605_27691_b200 as knng
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    knng.lib()
+    ctx = knng.context()
+    assert ctx.device_count >= ws, f"{ws} ranks need {ws} visible GPUs"
+    stream = torch.cuda.ExternalStream(ctx.stream(local), device=f"cuda:{local}")
+    n = args.per_gpu * ws
+    t0 = time.time()
+    x_host = knng.gen_random_dataset(n, DIMS, "clustered", 42, 16)
+    gen_s = time.time() - t0
+    workload = (f"C4-regime weak scaling: {ws} x 1M x 128-d clustered(16) fp32, k=32, "
+                f"build_distributed P={ws} M=2 (partition, local NN-descent, tree refine, "
+                f"grouped merge, flat refine; beam 128 / 96 entries), one process per GPU")
+    ref_name = f"dist_p{ws}_{ws}m_clustered16_k32"
+    pinned = torch.empty(x_host.shape, dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = x_host
+    x_np_pinned = pinned.numpy()
+    x_dev = pinned.to(f"cuda:{local}")
+    torch.cuda.synchronize()
+    cfg = knng.RefineConfig(ranks=ws, groups=2, k=K, seed=1, nn=knng.NnDescentParams(k=K, seed=1),
+                            search=knng.SearchParams(k_s=K, beam_width=128, num_entry_points=96,
+                                                     seed=1))
+    ag = knng.torch_allgather()
+
+    def step(x):
+        return knng.build_distributed_rank(x, cfg, rank, ws, ag, device=local)
+
+    ramp = []
+    t_ramp = time.time()
+    while not args.no_ramp and len(ramp) < 12:
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        step(x_dev)
+        torch.cuda.synchronize()
+        el, = allreduce(dist, [time.perf_counter() - t])
+        ramp.append(el)
+        stop = (len(ramp) >= 2 and abs(ramp[-1] - ramp[-2]) <= 0.05 * ramp[-2]) or \
+            time.time() - t_ramp > 60
+        stop, = allreduce(dist, [1.0 if stop else 0.0])
+        if stop:
+            break
+    for _ in range(args.warmup):
+        step(x_dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    sampler = ClockSampler(ws) if rank == 0 else None
+    if sampler:
+        sampler.__enter__()
+        sampler.wait_first(10.0)
+    step(x_dev)
+    barrier(dist)
+    torch.cuda.synchronize()
+    launches0 = knng.kernel_launches()
+    with torch.cuda.stream(stream):
+        ev[0].record(stream)
+    res = None
+    for i in range(args.steps):
+        res = step(x_dev)
+        with torch.cuda.stream(stream):
+            ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    launches = knng.kernel_launches() - launches0
+    barrier(dist)
+    if sampler:
+        sampler.__exit__()
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    dev_ms = ev[0].elapsed_time(ev[args.steps]) / args.steps
+    ms, = allreduce(dist, [dev_ms])
+    step_ms_max = allreduce(dist, step_ms)
+    launches_all, = allreduce(dist, [launches], op="sum")
+    phases = allreduce(dist, [res.partition_s, res.local_s, res.tree_s, res.merge_s, res.flat_s,
+                              res.etc_s])
+
+    # e2e through the public API: pinned host dataset in, this rank's rows out
+    e2e = []
+    for _ in range(max(1, min(args.steps, 3))):
+        barrier(dist)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        out = step(x_np_pinned)
+        e2e.append(time.perf_counter() - t)
+    e2e_ms, = allreduce(dist, [1000.0 * statistics.mean(e2e)])
+    h2d = ws * n * DIMS * 4        # every rank receives the dataset
+    d2h = n * K * 8 + n * 4        # all ranks' rows: ids + dists + external row ids
+    del out
+
+    # recall@10 on ~10K sampled rows (each rank samples its own rows)
+    rows_ext = res.rows.cpu().numpy().astype(np.uint64)
+    rng = np.random.default_rng(12345 + rank)
+    pick = np.sort(rng.choice(len(rows_ext), size=min(len(rows_ext), 10000 // ws), replace=False))
+    gt, _ = knng.brute_force_knng(x_dev, 10, rows=rows_ext[pick], device=local)
+    gt = gt.cpu().numpy() if hasattr(gt, "cpu") else gt
+    mine = res.graph.ids.cpu().numpy()[pick, :10]
+    hits = sum(len(np.intersect1d(mine[i], gt[i])) for i in range(len(pick)))
+    hits_all, cnt_all = allreduce(dist, [hits, len(pick)], op="sum")
+    rec = hits_all / (cnt_all * 10.0)
+    ref_rec, ref_src = reference_recall(ref_name)
+
+    # local-build phase efficiency: rank 0's share built alone, ranks idle
+    local_phase = None
+    barrier(dist)
+    if rank == 0:
+        part = knng.partition_dataset(x_dev, ws, cfg.seed, gather=False, device=local)
+        lo, hi = int(part.offsets[0]), int(part.offsets[1])
+        idx = torch.from_numpy(part.to_external[lo:hi].astype(np.int64)).to(f"cuda:{local}")
+        xs = x_dev.index_select(0, idx).contiguous()
+        p0 = knng.NnDescentParams(k=K, seed=1)
+        knng.nn_descent(xs, p0)
+        t1 = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            knng.nn_descent(xs, p0)
+            torch.cuda.synchronize()
+            t1.append(time.perf_counter() - t)
+        one = min(t1)
+        local_phase = {"ms": 1000 * phases[1], "single_gpu_same_share_ms": 1000 * one,
+                       "efficiency": one / phases[1] if phases[1] else None,
+                       "note": "rank-0 share built alone on one GPU in the same run; local phase "
+                               "= max over ranks"}
+    barrier(dist)
+    if rank == 0:
+        line = {"metric": METRIC, "value": n / (ms / 1000.0), "unit": "points/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (reference generator gen_random_dataset, seed 42)",
+                "config": {"workload": workload, "n": n, "dims": DIMS, "k": K,
+                           "l2_flush": "inputs larger than L2 (dataset %.0f MB)" % (n * DIMS * 4 / 1e6),
+                           "parallelism": f"partition x{ws}, one process per GPU"},
+                "recall_at_10": rec, "reference_recall_at_10": ref_rec,
+                "reference_recall_source": ref_src, "recall_rows": int(cnt_all),
+                "e2e": {"value": n / (e2e_ms / 1000.0), "unit": "points/s", "ms_per_step": e2e_ms,
+                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "clocks": sampler.summary() if sampler else None, "setup_gen_s": gen_s,
+                "clock_ramp_ms": [round(1000 * t, 1) for t in ramp],
+                "step_ms": [round(t, 2) for t in step_ms_max],
+                "phases_s": dict(zip(("partition", "local", "tree", "merge", "flat", "etc"),
+                                     phases)),
+                "comm": {"gets": len(res.comm_log),
+                         "wire_bytes": sum(c.bytes for c in res.comm_log)},
+                "gpu_launches": int(launches_all), "local_phase": local_phase}
+        print(json.dumps(line), flush=True)
     barrier(dist)
 
 

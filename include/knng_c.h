@@ -229,6 +229,26 @@ knng_status knng_build_distributed(knng_ctx* ctx, const knng_dataset* ds,
                                    const knng_refine_config* cfg, knng_graph* out,
                                    knng_dist_result* result, uint32_t* snap_ids,
                                    float* snap_dists, uint64_t snap_cap);
+/* Host transport for one-process-per-GPU builds: an all-gather -- out =
+ * world_size consecutive blocks of `bytes`, in rank order.  Return 0 on
+ * success (nonzero aborts the build with KNNG_EWORLD). */
+typedef int (*knng_allgather_fn)(void* user, const void* in, uint64_t bytes, void* out);
+/* One rank of build_distributed (refine.cpp:504-586) in this process, for
+ * launches with one process per GPU (torchrun).  Collective: every rank calls
+ * it with the same full dataset and config; the partition is recomputed
+ * identically per rank, the rank's block is built and refined on `device`,
+ * and published regions are shared as CUDA IPC handles exchanged with
+ * `allgather` (pulls stay one-sided NVLink copies, RankWorld::one_sided_get).
+ * Outputs (ceil(N / world_size) rows capacity, host or device per out_mem):
+ * the rank's rows of the final graph in external ids (rows x k) and each
+ * row's external id; *rows_out = the rank's row count.  result->comm_log
+ * covers every rank's gets. */
+knng_status knng_build_distributed_rank(knng_ctx* ctx, int device, uint64_t rank,
+                                        uint64_t world_size, knng_allgather_fn allgather,
+                                        void* user, const knng_dataset* ds,
+                                        const knng_refine_config* cfg, uint32_t* out_ids,
+                                        float* out_dists, uint32_t* out_rows, int out_mem,
+                                        uint64_t* rows_out, knng_dist_result* result);
 /* World-level drivers from given local graphs (internal global ids):
  * mode 0 = binary_tree_refine -> grouped_merge -> flat_refine,
  * mode 1 = all_to_all_refine (refine.hpp:117-136).  x_perm: rows in internal

@@ -670,6 +670,33 @@ knng_status knng_build_distributed(knng_ctx* ctx, const knng_dataset* ds,
   });
 }
 
+knng_status knng_build_distributed_rank(knng_ctx* ctx, int device, uint64_t rank,
+                                        uint64_t world_size, knng_allgather_fn allgather,
+                                        void* user, const knng_dataset* ds,
+                                        const knng_refine_config* cfg, uint32_t* out_ids,
+                                        float* out_dists, uint32_t* out_rows, int out_mem,
+                                        uint64_t* rows_out, knng_dist_result* result) {
+  return guard([&] {
+    require(ctx && ds && cfg && out_ids && out_dists && out_rows && allgather,
+            "build_distributed: null argument");
+    ctx->runner(device);  // the device belongs to this context
+    check_ds(ds);
+    RefineCfg c = to_cfg(cfg);
+    c.ranks = world_size;
+    HostTransport t;
+    t.user = user;
+    t.allgather = allgather;
+    DistResult res;
+    const uint64_t rows = build_distributed_rank(
+        device, (size_t)rank, (size_t)world_size, t, static_cast<const float*>(ds->data),
+        ds->mem == KNNG_MEM_DEVICE, ds->n, (int)ds->dims, c, out_ids, out_dists, out_rows,
+        out_mem == KNNG_MEM_DEVICE, &res);
+    if (rows_out) *rows_out = rows;
+    ctx->last_log = res.comm_log;
+    fill_dist_result(res, result);
+  });
+}
+
 knng_status knng_refine(knng_ctx* ctx, const float* x_perm, uint64_t n, uint64_t dims,
                         const knng_refine_config* cfg, const uint64_t* offsets, uint32_t* ids,
                         float* dists, int mode, knng_dist_result* result) {

@@ -53,7 +53,7 @@ __device__ __forceinline__ u32 bucket_hash(u32 u, u32 v, u32 nb) {
   return x % nb;
 }
 
-// Lock-free offer given a snapshot of its bucket.  The bucket keeps its W
+// Lock-free offers (k_offer) given a snapshot of the bucket.  The bucket keeps its W
 // smallest distinct (dist,id) keys in ascending order: each step atomicMin's
 // the carried key into one slot and carries the larger of (old, key) onward.
 // Slots only decrease, so whatever the interleaving the final bucket is the W
@@ -62,24 +62,6 @@ __device__ __forceinline__ u32 bucket_hash(u32 u, u32 v, u32 nb) {
 // smallest, a key equal to a snapshot entry is already buffered (or displaced
 // by smaller ones), and every slot before the snapshot insertion position
 // already holds a smaller key, so the cascade starts there.
-__device__ __forceinline__ void offer_from(u64* __restrict__ bucket, u32 ways, u64 key,
-                                           const u64 (&snap)[4]) {
-  u32 pos = 0;
-#pragma unroll
-  for (u32 w = 0; w < 4; ++w) {
-    if (w < ways && snap[w] == key) return;
-    pos += (w < ways && snap[w] < key) ? 1u : 0u;
-  }
-  if (pos >= ways) return;
-  for (u32 w = pos; w < ways; ++w) {
-    const u64 old = atomicMin(reinterpret_cast<unsigned long long*>(bucket + w),
-                              (unsigned long long)key);
-    if (old == key) return;
-    key = old > key ? old : key;
-    if (key == kEmptyKey) return;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // k_join_lists
 // ---------------------------------------------------------------------------
@@ -132,7 +114,7 @@ __global__ __launch_bounds__(256) void k_join_lists(u64 n, u32 k, u32 B, int RMA
 // ---------------------------------------------------------------------------
 // k_offer
 // ---------------------------------------------------------------------------
-constexpr int kOfferBatch = 4;
+constexpr int kOfferBatch = 2;  // offers per thread (rounds keep their atomics independent)
 
 __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
                                                const u32* __restrict__ q_tgt,
@@ -150,7 +132,7 @@ __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
       const u32 e0 = e_base + threadIdx.x;
       u64 key[kOfferBatch];
       u64* bk[kOfferBatch];
-      u64 snap[kOfferBatch][4];
+      u32 pos[kOfferBatch];
 #pragma unroll
       for (int i = 0; i < kOfferBatch; ++i) {
         const u32 e = e0 + i * blockDim.x;
@@ -161,25 +143,54 @@ __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
           bk[i] = slots + (u64)tgt * S + (u64)bucket_hash(tgt, key_id(key[i]), nb) * ways;
         }
       }
+      // L2-coherent snapshots (L1 lines would go stale under the atomics);
+      // the cascade of each offer starts at its snapshot insertion position
 #pragma unroll
       for (int i = 0; i < kOfferBatch; ++i) {
+        pos[i] = 4;
         if (!bk[i]) continue;
+        u64 sn[4];
         if (ways == 4) {
-          // L2-coherent snapshot (L1 lines would go stale under the atomics)
           const ulonglong2 lo = __ldcg(reinterpret_cast<const ulonglong2*>(bk[i]));
           const ulonglong2 hi = __ldcg(reinterpret_cast<const ulonglong2*>(bk[i] + 2));
-          snap[i][0] = lo.x;
-          snap[i][1] = lo.y;
-          snap[i][2] = hi.x;
-          snap[i][3] = hi.y;
+          sn[0] = lo.x;
+          sn[1] = lo.y;
+          sn[2] = hi.x;
+          sn[3] = hi.y;
         } else {
 #pragma unroll
-          for (u32 w = 0; w < 4; ++w) snap[i][w] = w < ways ? __ldcg(bk[i] + w) : kEmptyKey;
+          for (u32 w = 0; w < 4; ++w) sn[w] = w < ways ? __ldcg(bk[i] + w) : kEmptyKey;
+        }
+        u32 p = 0;
+        bool dup = false;
+#pragma unroll
+        for (u32 w = 0; w < 4; ++w) {
+          dup |= (w < ways && sn[w] == key[i]);
+          p += (w < ways && sn[w] < key[i]) ? 1u : 0u;
+        }
+        pos[i] = (dup || p >= ways) ? 4u : p;
+      }
+      // rounds: one independent atomicMin per live offer (pipelined), then
+      // carry the larger of (old, key) to the next slot (the cascade above)
+#pragma unroll
+      for (int round = 0; round < 4; ++round) {
+        u64 old[kOfferBatch];
+#pragma unroll
+        for (int i = 0; i < kOfferBatch; ++i)
+          if (pos[i] < ways)
+            old[i] = atomicMin(reinterpret_cast<unsigned long long*>(bk[i] + pos[i]),
+                               (unsigned long long)key[i]);
+#pragma unroll
+        for (int i = 0; i < kOfferBatch; ++i) {
+          if (pos[i] >= ways) continue;
+          if (old[i] == key[i]) {
+            pos[i] = 4;
+            continue;
+          }
+          key[i] = old[i] > key[i] ? old[i] : key[i];
+          pos[i] = key[i] == kEmptyKey ? 4u : pos[i] + 1;
         }
       }
-#pragma unroll
-      for (int i = 0; i < kOfferBatch; ++i)
-        if (bk[i]) offer_from(bk[i], ways, key[i], snap[i]);
       __syncwarp();
     }
   }
@@ -251,13 +262,14 @@ struct Smem {
   }
   __device__ int* rb(int q) const { return reinterpret_cast<int*>(desc + q * desc_bytes); }
   __device__ int* tb(int q) const { return rb(q) + (G + 1); }
-  __device__ int* dhdr(int q) const { return rb(q) + 2 * (G + 1); }  // [0] meta, [1] jb, [2] je
-  __device__ u32* rowid(int q) const { return reinterpret_cast<u32*>(rb(q) + 2 * (G + 1) + 4); }
+  // [0] meta, [1] jb, [2] je, [3] first tile of point jb, [4] next point, [5] its first tile
+  __device__ int* dhdr(int q) const { return rb(q) + 2 * (G + 1); }
+  __device__ u32* rowid(int q) const { return reinterpret_cast<u32*>(rb(q) + 2 * (G + 1) + 8); }
   __device__ float* x(int b) const { return x0 + b * xstride; }
 };
 
 __host__ __device__ inline size_t desc_slot_bytes(int RB) {
-  return ((size_t)(2 * (G + 1) + 4) * 4 + (size_t)RB * 4 + 15) & ~size_t(15);
+  return ((size_t)(2 * (G + 1) + 8) * 4 + (size_t)RB * 4 + 15) & ~size_t(15);
 }
 
 __device__ __forceinline__ Smem carve(unsigned char* base, int RMAX, int RB, int DCP) {
@@ -313,20 +325,42 @@ __device__ bool load_chunk(const JoinArgs& a, const Smem& s, int m) {
   return true;
 }
 
-// Thread 0 packs points [jb, ..) of meta slot m into desc slot q.
-__device__ void form_batch(const JoinArgs& a, const Smem& s, int q, int m, int jb) {
+// Thread 0 packs the tiles of meta slot m, starting at tile t0 of point jb,
+// into desc slot q: whole points while rows fit, and the tile budget is filled
+// exactly -- a point whose tiles do not all fit is split, the rest of it opens
+// the next batch (its rows are staged in both; every tile is computed once).
+__device__ void form_batch(const JoinArgs& a, const Smem& s, int q, int m, int jb, int t0) {
   if (threadIdx.x == 0) {
     const int np = s.mhdr(m)[1];
-    int rows = 0, tiles = 0, je = jb;
+    int rows = 0, tiles = 0, je = jb, jn = np, tn = 0;
     while (je < np) {
       const u32 c = s.cnt(m)[je];
-      const int t = tiles_of(c);
-      const int na = t ? (int)(c >> 16) : 0;
-      if (je > jb && (rows + na > a.RB || tiles + t > kMaxTiles)) break;
+      const int tt = tiles_of(c);
+      const int avail = tt - (je == jb ? t0 : 0);
+      const int na = tt ? (int)(c >> 16) : 0;
+      if (je > jb && rows + na > a.RB) {  // rows full: the next batch opens at je
+        jn = je;
+        break;
+      }
+      if (tiles + avail > kMaxTiles) {
+        const int take = kMaxTiles - tiles;
+        if (take <= 0) {
+          jn = je;
+          break;
+        }
+        s.rb(q)[je] = rows;
+        s.tb(q)[je] = tiles;
+        rows += na;
+        tiles += take;
+        jn = je;
+        tn = (je == jb ? t0 : 0) + take;
+        ++je;
+        break;
+      }
       s.rb(q)[je] = rows;
       s.tb(q)[je] = tiles;
       rows += na;
-      tiles += t;
+      tiles += avail;
       ++je;
     }
     s.rb(q)[je] = rows;
@@ -334,6 +368,9 @@ __device__ void form_batch(const JoinArgs& a, const Smem& s, int q, int m, int j
     s.dhdr(q)[0] = m;
     s.dhdr(q)[1] = jb;
     s.dhdr(q)[2] = je;
+    s.dhdr(q)[3] = t0;
+    s.dhdr(q)[4] = jn;
+    s.dhdr(q)[5] = tn;
   }
 }
 
@@ -390,7 +427,7 @@ __device__ __forceinline__ Tile decode_tile(const Smem& s, int q, int t) {
   const u32 c = s.cnt(m)[j];
   const int nn = c & 0xffff, na = c >> 16;
   const int rt = (nn + 3) >> 2, no = na - nn, cto = (no + 3) >> 2;
-  int lt = t - s.tb(q)[j];
+  int lt = t - s.tb(q)[j] + (j == jb ? s.dhdr(q)[3] : 0);
   T.pt = j;
   T.nn = nn;
   T.no = no;
@@ -430,7 +467,7 @@ __global__ __launch_bounds__(kJT, 1) void k_join(JoinArgs a) {
   // prologue: first chunk, first batch, first dim chunk
   if (!load_chunk(a, s, 0)) return;
   int cq = 0, cc0 = 0, cbuf = 0;  // current unit: desc slot, dim offset, buffer
-  form_batch(a, s, 0, 0, 0);
+  form_batch(a, s, 0, 0, 0, 0);
   __syncthreads();
   fill_rowids(a, s, 0);
   __syncthreads();
@@ -446,12 +483,12 @@ __global__ __launch_bounds__(kJT, 1) void k_join(JoinArgs a) {
       nc0 = 0;
       nq = cq ^ 1;
       const int m = s.dhdr(cq)[0];
-      const int je = s.dhdr(cq)[2];
-      if (je < s.mhdr(m)[1]) {
-        form_batch(a, s, nq, m, je);
+      const int jn = s.dhdr(cq)[4], tn = s.dhdr(cq)[5];
+      if (jn < s.mhdr(m)[1]) {
+        form_batch(a, s, nq, m, jn, tn);
       } else if (load_chunk(a, s, m ^ 1)) {
         if (m ^ 1) q_used1 = 0; else q_used0 = 0;
-        form_batch(a, s, nq, m ^ 1, 0);
+        form_batch(a, s, nq, m ^ 1, 0, 0);
       } else {
         have_next = false;
       }
@@ -596,7 +633,7 @@ __global__ __launch_bounds__(kJT, 1) void k_join(JoinArgs a) {
           }
         }
       }
-      if (s.dhdr(cq)[2] >= s.mhdr(m)[1] && tid == 0) {  // chunk complete
+      if (s.dhdr(cq)[4] >= s.mhdr(m)[1] && tid == 0) {  // chunk complete
         a.q_fill[chunk] = qu + btot;
         my_offers += qu + btot;
       }

@@ -51,7 +51,7 @@ struct Shared {
   int d = 0;
   uint64_t k = 0, ks = 0, od = 0, groups = 1, levels = 0;
   SearchParamsDev sp;
-  ThreadWorld* world = nullptr;
+  World* world = nullptr;
 };
 
 struct RankState {
@@ -271,10 +271,30 @@ void refine_rank(Shared& S, RankState& R, bool capture) {
   r.sync();
 }
 
+// local_build_rank refine.cpp:380-390: nn_descent on the rank's rows, seed
+// mix(nn.seed, rank) for P > 1, ids shifted to internal global ids
+void local_build_rank(Shared& S, const RefineCfg& cfg, RankState& R) {
+  Runner& r = *R.runner;
+  DeviceGuard g(r.device);
+  const double t = now_s();
+  const uint64_t p = S.offsets.size() - 1;
+  NndParams np = cfg.nn;
+  np.k = (uint32_t)cfg.k;
+  np.seed = p == 1 ? cfg.nn.seed : mix_seed(cfg.nn.seed, R.rank);  // refine.cpp:385
+  DBuf<u32> flags(r, R.n_local);
+  nn_descent_device(r, DevRows{R.local_x.p, R.n_local, S.d}, np, R.keys.p, flags.p, &R.nst,
+                    true);
+  shift_ids_device(r, R.keys.p, R.n_local * S.k, (int64_t)S.offsets[R.rank]);
+  r.sync();
+  R.local_t = now_s() - t;
+  trace(R.rank, "local");
+  if (cfg.capture_snapshots) snapshot(R, S.k);
+}
+
 // run body(rank) on one thread per rank; first genuine failure rethrown
 // (RankRunner distsim.hpp:113-153)
 template <class Body>
-void run_ranks(ThreadWorld& world, size_t p, Body&& body) {
+void run_ranks(World& world, size_t p, Body&& body) {
   std::vector<std::exception_ptr> errors(p);
   std::vector<std::thread> threads;
   threads.reserve(p);
@@ -348,7 +368,7 @@ void translate_all(Runner& r0, std::vector<RankState>& ranks, const std::vector<
   r0.sync();
 }
 
-void fill_result(Shared& S, std::vector<RankState>& ranks, ThreadWorld* world, DistResult* res) {
+void fill_result(Shared& S, std::vector<RankState>& ranks, World* world, DistResult* res) {
   if (!res) return;
   for (auto& R : ranks) {
     res->local_s = std::max(res->local_s, R.local_t);
@@ -447,26 +467,7 @@ void build_distributed(const std::vector<int>& devices, const float* X, bool x_o
   if (res) res->partition_s = now_s() - t0;
   trace(0, "partitioned");
 
-  auto local_build = [&](RankState& R) {
-    Runner& r = *R.runner;
-    DeviceGuard g(r.device);
-    const double t = now_s();
-    NndParams np = cfg.nn;
-    np.k = (uint32_t)cfg.k;
-    np.seed = p == 1 ? cfg.nn.seed : mix_seed(cfg.nn.seed, R.rank);  // refine.cpp:385
-    DBuf<u32> flags(r, R.n_local);
-    nn_descent_device(r, DevRows{R.local_x.p, R.n_local, d}, np, R.keys.p, flags.p, &R.nst,
-                      true);
-    if (slow_trace_on())
-      std::fprintf(stderr, "[knng slow] t %.1f rank %zu nnd returned\n", trace_clock_ms(), R.rank);
-    shift_ids_device(r, R.keys.p, R.n_local * S.k, (int64_t)offsets[R.rank]);
-    r.sync();
-    if (slow_trace_on())
-      std::fprintf(stderr, "[knng slow] t %.1f rank %zu shifted+synced\n", trace_clock_ms(), R.rank);
-    R.local_t = now_s() - t;
-    trace(R.rank, "local");
-    if (cfg.capture_snapshots) snapshot(R, S.k);
-  };
+  auto local_build = [&](RankState& R) { local_build_rank(S, cfg, R); };
 
   std::unique_ptr<ThreadWorld> world;
   if (p == 1) {
@@ -557,6 +558,76 @@ void refine_from_local(const std::vector<int>& devices, const float* X_perm, uin
     r.sync();
   }
   fill_result(S, ranks, &world, res);
+}
+
+uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const HostTransport& t,
+                                const float* X, bool x_on_device, uint64_t n, int d,
+                                const RefineCfg& cfg_in, uint32_t* out_ids, float* out_dists,
+                                uint32_t* out_rows, bool out_on_device, DistResult* res) {
+  RefineCfg cfg = cfg_in;
+  cfg.ranks = ranks;
+  require(rank < ranks, "build_distributed: rank out of range");
+  require(!(ranks == 0 || ranks > n), "partition_dataset: need 1 <= P <= N");
+  require(!cfg.capture_snapshots, "build_distributed: snapshots need the single-process driver");
+  // the rank state (and its runner/stream) is declared first so it outlives
+  // every buffer below that frees on its stream
+  std::vector<RankState> one(1);
+  RankState& R = one[0];
+  R.rank = rank;
+  R.runner = std::make_unique<Runner>(device);
+  Runner& r = *R.runner;
+  DeviceGuard g(r.device);
+  const double t0 = now_s();
+  g_trace_t0 = t0;
+  DBuf<float> xdev;
+  const float* Xd = X;
+  if (!x_on_device) {
+    xdev.alloc(r, n * d);
+    KNNG_CUDA(cudaMemcpyAsync(xdev.p, X, n * (uint64_t)d * 4, cudaMemcpyHostToDevice, r.stream));
+    Xd = xdev.p;
+  }
+  // every rank computes the same permutation (refine.cpp:86-126, bit-exact)
+  DBuf<u32> to_ext(r, n);
+  std::vector<uint64_t> offsets;
+  partition_device(r, n, (uint32_t)ranks, cfg.seed, to_ext.p, offsets);
+  validate_config(offsets, cfg);
+  Shared S = make_shared_state(cfg, offsets, d);
+  R.n_local = size_of(S, rank);
+  R.local_x.alloc(r, R.n_local * d);
+  R.keys.alloc(r, R.n_local * S.k);
+  gather_rows_device(r, Xd, d, to_ext.p + offsets[rank], R.n_local, R.local_x.p);
+  if (!x_on_device) xdev.release();
+  r.sync();
+  if (res) res->partition_s = now_s() - t0;
+  std::unique_ptr<ProcWorld> world;
+  if (ranks > 1) {
+    world = std::make_unique<ProcWorld>(ranks, rank, t);
+    S.world = world.get();
+  }
+  local_build_rank(S, cfg, R);
+  if (ranks > 1) refine_rank(S, R, false);
+  const double te = now_s();
+  if (out_on_device) {
+    translate_rows_device(r, R.keys.p, R.n_local, (u32)S.k, to_ext.p, offsets[rank], out_ids,
+                          out_dists, out_rows);
+  } else {
+    DBuf<u32> ti(r, R.n_local * S.k), tr(r, R.n_local);
+    DBuf<float> td(r, R.n_local * S.k);
+    translate_rows_device(r, R.keys.p, R.n_local, (u32)S.k, to_ext.p, offsets[rank], ti.p, td.p,
+                          tr.p);
+    KNNG_CUDA(cudaMemcpyAsync(out_ids, ti.p, R.n_local * S.k * 4, cudaMemcpyDeviceToHost,
+                              r.stream));
+    KNNG_CUDA(cudaMemcpyAsync(out_dists, td.p, R.n_local * S.k * 4, cudaMemcpyDeviceToHost,
+                              r.stream));
+    KNNG_CUDA(cudaMemcpyAsync(out_rows, tr.p, R.n_local * 4, cudaMemcpyDeviceToHost, r.stream));
+  }
+  r.sync();
+  if (res) {
+    fill_result(S, one, nullptr, res);
+    res->etc_s = now_s() - te;
+    if (world) res->comm_log = world->gather_comm_log();
+  }
+  return R.n_local;
 }
 
 }  // namespace knng_b200

@@ -57,6 +57,18 @@ void build_distributed(const std::vector<int>& devices, const float* X, bool x_o
                        uint64_t n, int d, const RefineCfg& cfg, uint32_t* out_ids,
                        float* out_dists, bool out_on_device, DistResult* res);
 
+// One rank of build_distributed in this process (one process per GPU):
+// every rank passes the same full dataset; the partition is recomputed
+// identically, the rank builds and refines its block on `device`, and the
+// cross-rank pulls go through a ProcWorld over the caller's host transport.
+// Outputs: the rank's rows in external ids (rows x k) and each row's external
+// id; returns the row count (<= ceil(n / ranks)).  Collective: every rank of
+// the transport must call it with the same arguments.
+uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const HostTransport& t,
+                                const float* X, bool x_on_device, uint64_t n, int d,
+                                const RefineCfg& cfg, uint32_t* out_ids, float* out_dists,
+                                uint32_t* out_rows, bool out_on_device, DistResult* res);
+
 // Refinement only, from given local graphs (internal global ids, rank blocks
 // at offsets) -- the world-level drivers binary_tree_refine -> grouped_merge
 // -> flat_refine (mode 0) or all_to_all_refine (mode 1), refine.hpp:117-136.

@@ -171,10 +171,13 @@ __global__ __launch_bounds__(256) void k_merge_rows(const u64* akeys, const u32*
 
 // translate_to_external: rows [0, n) of the internal-order graph (row g is
 // internal id g) -> external row to_external[g], ids mapped, re-sorted.
+// row g of keys is internal row row_base + g; scattered to its external row
+// (full graph) or kept at g with its external row id in out_rows (compact)
 __global__ __launch_bounds__(256) void k_translate(const u64* __restrict__ keys, u64 n, u32 k,
                                                    const u32* __restrict__ to_ext,
                                                    u32* __restrict__ out_ids,
-                                                   float* __restrict__ out_d) {
+                                                   float* __restrict__ out_d, u64 row_base,
+                                                   u32* __restrict__ out_rows) {
   const unsigned lane = lane_id();
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
   for (u64 g = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); g < n; g += warps) {
@@ -184,7 +187,9 @@ __global__ __launch_bounds__(256) void k_translate(const u64* __restrict__ keys,
       key = ((kk >> 32) << 32) | to_ext[key_id(kk)];
     }
     key = warp_sort32(key);
-    const u64 dst = to_ext[g];
+    const u64 ext_row = to_ext[row_base + g];
+    const u64 dst = out_rows ? g : ext_row;
+    if (out_rows && lane == 0) out_rows[g] = (u32)ext_row;
     if (lane < k) {
       out_ids[dst * k + lane] = key_id(key);
       out_d[dst * k + lane] = key_dist(key);
@@ -290,7 +295,17 @@ void shift_ids_device(const Runner& r, uint64_t* keys, uint64_t count, int64_t d
 void translate_device(const Runner& r, const uint64_t* keys, uint64_t n, uint32_t k,
                       const uint32_t* to_ext, uint32_t* out_ids, float* out_d) {
   if (!n) return;
-  k_translate<<<warp_grid(r, n), 256, 0, r.stream>>>(keys, n, k, to_ext, out_ids, out_d);
+  k_translate<<<warp_grid(r, n), 256, 0, r.stream>>>(keys, n, k, to_ext, out_ids, out_d, 0,
+                                                     nullptr);
+  KNNG_LAUNCH_CHECK();
+}
+
+void translate_rows_device(const Runner& r, const uint64_t* keys, uint64_t rows, uint32_t k,
+                           const uint32_t* to_ext, uint64_t row_base, uint32_t* out_ids,
+                           float* out_d, uint32_t* out_rows) {
+  if (!rows) return;
+  k_translate<<<warp_grid(r, rows), 256, 0, r.stream>>>(keys, rows, k, to_ext, out_ids, out_d,
+                                                        row_base, out_rows);
   KNNG_LAUNCH_CHECK();
 }
 

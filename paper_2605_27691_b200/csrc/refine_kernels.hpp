@@ -30,6 +30,11 @@ void shift_ids_device(const Runner& r, uint64_t* keys, uint64_t count, int64_t d
 // translate_to_external refine.cpp:395-416 for an internal-order N x k graph.
 void translate_device(const Runner& r, const uint64_t* keys, uint64_t n, uint32_t k,
                       const uint32_t* to_ext, uint32_t* out_ids, float* out_d);
+// The same for internal rows [row_base, row_base + rows) of one rank, written
+// compactly: row g -> out row g, external row id -> out_rows[g].
+void translate_rows_device(const Runner& r, const uint64_t* keys, uint64_t rows, uint32_t k,
+                           const uint32_t* to_ext, uint64_t row_base, uint32_t* out_ids,
+                           float* out_d, uint32_t* out_rows);
 
 // Exact k-NN (brute_force_knng evalio.cpp:125-147) of rows[0..q) against all n
 // rows of X (self excluded), k <= 32; keys out q x k.

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -77,6 +78,33 @@ struct RegionCache {
 RegionCache& region_cache() {
   static RegionCache* c = new RegionCache();  // process lifetime (freed by the driver at exit)
   return *c;
+}
+
+// Imported IPC mappings, process-wide: the exporting ranks keep their region
+// buffers in their RegionCache, so a handle stays valid across builds and is
+// opened once (cudaIpcOpenMemHandle / Close cost milliseconds and synchronise).
+struct IpcMaps {
+  std::mutex mu;
+  std::map<std::string, void*> open;  // (device, handle bytes) -> mapped pointer
+  void* map(int dev, const unsigned char* handle) {
+    std::string key(reinterpret_cast<const char*>(handle), 64);
+    key.append(reinterpret_cast<const char*>(&dev), sizeof(dev));
+    std::lock_guard<std::mutex> l(mu);
+    auto it = open.find(key);
+    if (it != open.end()) return it->second;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    DeviceGuard g(dev);
+    KNNG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    open[key] = p;
+    return p;
+  }
+};
+
+IpcMaps& ipc_maps() {
+  static IpcMaps* m = new IpcMaps();
+  return *m;
 }
 
 }  // namespace
@@ -247,6 +275,159 @@ void ThreadWorld::abort(const std::string& reason) {
 std::vector<GetRecord> ThreadWorld::comm_log() const {
   std::lock_guard<std::mutex> l(mu_);
   return log_;
+}
+
+// ---------------------------------------------------------------------------
+// ProcWorld
+// ---------------------------------------------------------------------------
+ProcWorld::ProcWorld(size_t num_ranks, size_t rank, const HostTransport& t)
+    : num_ranks_(num_ranks), rank_(rank), t_(t) {
+  require(num_ranks >= 1 && rank < num_ranks, "RankWorld: rank out of range");
+  require(t.allgather != nullptr, "RankWorld: the process transport needs an allgather");
+  remote_.assign(num_ranks, {});
+}
+
+ProcWorld::~ProcWorld() {
+  for (auto& kv : mine_) {
+    for (Buf* b : {&kv.second.current, &kv.second.staged})
+      if (b->p) region_cache().release(b->dev, b->cap, b->p);
+  }
+}
+
+void ProcWorld::allgather(const void* in, uint64_t bytes, void* out) {
+  if (t_.allgather(t_.user, in, bytes, out) != 0) {
+    aborted_ = true;
+    throw WorldAborted("RankWorld: host transport failed (another rank aborted?)");
+  }
+}
+
+void ProcWorld::publish(size_t rank, const std::string& name, const void* dev_ptr,
+                        uint64_t bytes, uint64_t wire_bytes, Runner& r) {
+  require(rank == rank_, "RankWorld: a process publishes only its own rank's regions");
+  require(name.size() < sizeof(Entry::name), "RankWorld: region name too long");
+  if (aborted_) throw WorldAborted("RankWorld: aborted");
+  r.sync();
+  Slot& s = mine_[name];
+  if (s.last_epoch == epoch_)
+    throw WorldError("publish: region '" + name + "' already published by rank " +
+                     std::to_string(rank) + " in epoch " + std::to_string(epoch_));
+  Buf* target = s.has_current ? &s.staged : &s.current;
+  if (target->p && (target->cap < bytes || target->dev != r.device)) {
+    region_cache().release(target->dev, target->cap, target->p);
+    *target = Buf{};
+  }
+  DeviceGuard g(r.device);
+  if (!target->p && bytes) {
+    target->p = region_cache().acquire(r.device, bytes, &target->cap);
+    target->dev = r.device;
+  }
+  target->bytes = bytes;
+  target->wire = wire_bytes;
+  if (bytes) {
+    KNNG_CUDA(cudaMemcpyAsync(target->p, dev_ptr, bytes, cudaMemcpyDeviceToDevice, r.stream));
+    r.sync();
+  }
+  if (s.has_current) s.has_staged = true; else s.has_current = true;
+  s.last_epoch = epoch_;
+}
+
+void ProcWorld::barrier(size_t rank, Runner& r) {
+  require(rank == rank_, "RankWorld: rank out of range");
+  if (aborted_) throw WorldAborted("RankWorld: aborted");
+  r.sync();  // this rank's pulls and publishes are complete
+  for (auto& kv : mine_) {
+    Slot& s = kv.second;
+    if (s.has_staged) {
+      std::swap(s.current, s.staged);
+      s.has_staged = false;
+    }
+  }
+  ++epoch_;
+  // exchange the tables of current regions (the all-gather is the barrier)
+  std::vector<Entry> table(kMaxRegions);
+  std::memset(table.data(), 0, sizeof(Entry) * kMaxRegions);
+  int i = 0;
+  for (auto& kv : mine_) {
+    require(i < kMaxRegions, "RankWorld: too many regions");
+    const Buf& b = kv.second.current;
+    Entry& e = table[i++];
+    std::strncpy(e.name, kv.first.c_str(), sizeof(e.name) - 1);
+    e.bytes = b.bytes;
+    e.wire = b.wire;
+    e.cap = b.cap;
+    e.dev = b.dev;
+    e.valid = kv.second.has_current ? 1 : 0;
+    if (b.p) {
+      DeviceGuard g(b.dev);
+      cudaIpcMemHandle_t h;
+      KNNG_CUDA(cudaIpcGetMemHandle(&h, b.p));
+      std::memcpy(e.handle, &h, sizeof(h));
+    }
+  }
+  std::vector<Entry> all(kMaxRegions * num_ranks_);
+  allgather(table.data(), sizeof(Entry) * kMaxRegions, all.data());
+  for (size_t t = 0; t < num_ranks_; ++t)
+    remote_[t].assign(all.begin() + (std::ptrdiff_t)(t * kMaxRegions),
+                      all.begin() + (std::ptrdiff_t)((t + 1) * kMaxRegions));
+}
+
+uint64_t ProcWorld::get(size_t src, size_t target, const std::string& name, void* dst,
+                        Runner& r) {
+  require(src == rank_ && target < num_ranks_, "RankWorld: rank out of range");
+  if (aborted_) throw WorldAborted("RankWorld: aborted");
+  DeviceGuard g(r.device);
+  if (target == rank_) {
+    auto it = mine_.find(name);
+    if (it == mine_.end() || !it->second.has_current)
+      throw WorldError("one_sided_get: region '" + name + "' not published by rank " +
+                       std::to_string(target));
+    const Buf& b = it->second.current;
+    log_.push_back({src, target, name, b.wire, epoch_, b.bytes});
+    if (b.bytes)
+      KNNG_CUDA(cudaMemcpyAsync(dst, b.p, b.bytes, cudaMemcpyDeviceToDevice, r.stream));
+    return b.bytes;
+  }
+  const Entry* e = nullptr;
+  for (const Entry& x : remote_[target])
+    if (x.valid && name == x.name) e = &x;
+  if (!e)
+    throw WorldError("one_sided_get: region '" + name + "' not published by rank " +
+                     std::to_string(target));
+  log_.push_back({src, target, name, e->wire, epoch_, e->bytes});
+  if (!e->bytes) return 0;
+  void* p = ipc_maps().map(r.device, e->handle);
+  // the owner runs nothing: a copy-engine pull over NVLink
+  KNNG_CUDA(cudaMemcpyAsync(dst, p, e->bytes, cudaMemcpyDefault, r.stream));
+  return e->bytes;
+}
+
+void ProcWorld::abort(const std::string&) { aborted_ = true; }
+
+std::vector<GetRecord> ProcWorld::gather_comm_log() {
+  struct Rec {
+    uint64_t src, target, bytes, epoch, device_bytes;
+    char region[24];
+  };
+  const uint64_t mine = log_.size();
+  std::vector<uint64_t> counts(num_ranks_);
+  allgather(&mine, sizeof(mine), counts.data());
+  uint64_t mx = 0;
+  for (uint64_t c : counts) mx = std::max(mx, c);
+  std::vector<Rec> out(mx ? mx : 1), all((mx ? mx : 1) * num_ranks_);
+  std::memset(out.data(), 0, sizeof(Rec) * out.size());
+  for (uint64_t i = 0; i < mine; ++i) {
+    const GetRecord& g = log_[i];
+    out[i] = Rec{g.src, g.target, g.bytes, g.epoch, g.device_bytes, {0}};
+    std::strncpy(out[i].region, g.region.c_str(), sizeof(out[i].region) - 1);
+  }
+  allgather(out.data(), sizeof(Rec) * out.size(), all.data());
+  std::vector<GetRecord> res;
+  for (size_t t = 0; t < num_ranks_; ++t)
+    for (uint64_t i = 0; i < counts[t]; ++i) {
+      const Rec& x = all[t * out.size() + i];
+      res.push_back({x.src, x.target, x.region, x.bytes, x.epoch, x.device_bytes});
+    }
+  return res;
 }
 
 }  // namespace knng_b200

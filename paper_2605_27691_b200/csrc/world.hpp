@@ -40,23 +40,39 @@ struct GetRecord {
 enum class RegionKind : uint8_t { dataset = 0, knng = 1, sgraph = 2, result = 3 };
 uint64_t wire_region_size(RegionKind kind, uint64_t rows, uint64_t cols, bool u8_elems = false);
 
-class ThreadWorld {
+// The refine phase's view of the transport (RankWorld's operations).
+class World {
+ public:
+  virtual ~World() = default;
+  virtual size_t num_ranks() const = 0;
+  virtual void publish(size_t rank, const std::string& name, const void* dev_ptr, uint64_t bytes,
+                       uint64_t wire_bytes, Runner& r) = 0;
+  // Copies the target's current snapshot into dst (on r's device/stream).
+  virtual uint64_t get(size_t src, size_t target, const std::string& name, void* dst,
+                       Runner& r) = 0;
+  virtual void barrier(size_t rank, Runner& r) = 0;
+  virtual void abort(const std::string& reason) = 0;
+  virtual std::vector<GetRecord> comm_log() const = 0;
+};
+
+// All ranks are host threads of this process (run_ranks, distsim.hpp:113-198).
+class ThreadWorld : public World {
  public:
   ThreadWorld(size_t num_ranks, std::chrono::milliseconds watchdog = std::chrono::seconds(600));
-  ~ThreadWorld();
+  ~ThreadWorld() override;
 
-  size_t num_ranks() const { return num_ranks_; }
+  size_t num_ranks() const override { return num_ranks_; }
   uint64_t epoch() const;
 
   void publish(size_t rank, const std::string& name, const void* dev_ptr, uint64_t bytes,
-               uint64_t wire_bytes, Runner& r);
-  // Copies the target's current snapshot into dst (on r's device/stream).
-  uint64_t get(size_t src, size_t target, const std::string& name, void* dst, Runner& r);
+               uint64_t wire_bytes, Runner& r) override;
+  uint64_t get(size_t src, size_t target, const std::string& name, void* dst,
+               Runner& r) override;
   uint64_t region_bytes(size_t target, const std::string& name);
-  void barrier(size_t rank, Runner& r);
-  void abort(const std::string& reason);
+  void barrier(size_t rank, Runner& r) override;
+  void abort(const std::string& reason) override;
   bool aborted() const;
-  std::vector<GetRecord> comm_log() const;
+  std::vector<GetRecord> comm_log() const override;
 
  private:
   struct Buf {
@@ -86,6 +102,66 @@ class ThreadWorld {
   size_t arrived_ = 0;
   bool aborted_ = false;
   std::string reason_;
+};
+
+// One rank per process (one process per GPU, e.g. torchrun).  Regions live in
+// this process's device buffers; at every barrier the ranks all-gather their
+// tables of current regions (name, CUDA IPC handle, sizes) through the host
+// transport the caller supplies, and a get maps the target's buffer once
+// (cudaIpcOpenMemHandle, cached) and pulls it with a device-to-device copy over
+// NVLink.  A region becomes visible to other ranks at the next barrier -- the
+// refine phase only reads regions after the barrier that follows their
+// publish, so this matches RankWorld for the reference's schedule.
+struct HostTransport {
+  void* user = nullptr;
+  // out = num_ranks consecutive blocks of `bytes`, in rank order; 0 = success
+  int (*allgather)(void* user, const void* in, uint64_t bytes, void* out) = nullptr;
+};
+
+class ProcWorld : public World {
+ public:
+  ProcWorld(size_t num_ranks, size_t rank, const HostTransport& t);
+  ~ProcWorld() override;
+
+  size_t num_ranks() const override { return num_ranks_; }
+  void publish(size_t rank, const std::string& name, const void* dev_ptr, uint64_t bytes,
+               uint64_t wire_bytes, Runner& r) override;
+  uint64_t get(size_t src, size_t target, const std::string& name, void* dst,
+               Runner& r) override;
+  void barrier(size_t rank, Runner& r) override;
+  void abort(const std::string& reason) override;
+  std::vector<GetRecord> comm_log() const override { return log_; }
+  // all ranks' gets (collective: every rank must call it)
+  std::vector<GetRecord> gather_comm_log();
+
+  static constexpr int kMaxRegions = 8;
+  struct Entry {  // fixed-size record exchanged at barriers
+    char name[24];
+    unsigned char handle[64];  // cudaIpcMemHandle_t
+    uint64_t bytes, wire, cap;
+    int32_t dev, valid;
+  };
+
+ private:
+  struct Buf {
+    void* p = nullptr;
+    uint64_t bytes = 0, cap = 0, wire = 0;
+    int dev = 0;
+  };
+  struct Slot {
+    Buf current, staged;
+    bool has_current = false, has_staged = false;
+    uint64_t last_epoch = ~0ull;
+  };
+  void allgather(const void* in, uint64_t bytes, void* out);
+
+  const size_t num_ranks_, rank_;
+  HostTransport t_;
+  std::map<std::string, Slot> mine_;
+  std::vector<std::vector<Entry>> remote_;  // [rank][region]
+  std::vector<GetRecord> log_;
+  uint64_t epoch_ = 0;
+  bool aborted_ = false;
 };
 
 }  // namespace knng_b200

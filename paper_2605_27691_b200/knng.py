@@ -155,6 +155,10 @@ _SIGS = {
     "knng_build_distributed": (C.c_int, [_vp, C.POINTER(_Dataset), C.POINTER(_RefineConfig),
                                          C.POINTER(_Graph), C.POINTER(_DistResult), _vp, _vp,
                                          _u64]),
+    "knng_build_distributed_rank": (C.c_int, [_vp, C.c_int, _u64, _u64, _vp, _vp,
+                                              C.POINTER(_Dataset), C.POINTER(_RefineConfig), _vp,
+                                              _vp, _vp, C.c_int, C.POINTER(_u64),
+                                              C.POINTER(_DistResult)]),
     "knng_refine": (C.c_int, [_vp, _vp, _u64, _u64, C.POINTER(_RefineConfig), _vp, _vp, _vp,
                               C.c_int, C.POINTER(_DistResult)]),
     "knng_last_comm_log": (C.c_int, [_vp, _vp, _u64, C.POINTER(_u64)]),
@@ -738,6 +742,75 @@ def build_distributed(x, cfg: RefineConfig) -> DistBuildResult:
         out_r.snapshots = [(lab, KnnGraph(snap_i[s], snap_d[s]))
                            for s, lab in enumerate(labels[:res.num_snapshots])]
     return out_r
+
+
+# knng_allgather_fn: int (*)(void* user, const void* in, uint64_t bytes, void* out)
+_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+
+
+def torch_allgather(group=None):
+    """Host transport for build_distributed_rank over torch.distributed: an
+    all-gather of CPU byte tensors (use a gloo group; the default group if it
+    is gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(inp, nbytes):
+        buf = torch.frombuffer(bytearray(C.string_at(inp, nbytes)), dtype=torch.uint8)
+        outs = [torch.empty(nbytes, dtype=torch.uint8)
+                for _ in range(dist.get_world_size(group))]
+        dist.all_gather(outs, buf, group=group)
+        return torch.cat(outs).numpy().tobytes()
+    return fn
+
+
+@dataclasses.dataclass
+class RankBuildResult(DistBuildResult):
+    """This rank's part of build_distributed: graph rows + their external ids."""
+    rows: Optional[object] = None
+
+
+def build_distributed_rank(x, cfg: RefineConfig, rank: int, world_size: int,
+                           allgather=None, device: Optional[int] = None) -> RankBuildResult:
+    """One rank of build_distributed (refine.cpp:504-586) in this process, for
+    one process per GPU.  Collective over `allgather(bytes_in, nbytes) ->
+    bytes_out` (default: torch_allgather() on the default group).  Every rank
+    passes the same full dataset; returns the rank's rows (external ids) and
+    their external row ids (graph.ids[i] is the neighbor list of row rows[i])."""
+    x = _as_rows(x)
+    n = x.shape[0]
+    k = cfg.k
+    cap = -(-n // world_size)
+    out_i = _empty_like_mem(x, (cap, k), np.uint32)
+    out_d = _empty_like_mem(x, (cap, k), np.float32)
+    out_r = _empty_like_mem(x, (cap,), np.uint32)
+    ag = allgather or torch_allgather()
+    err = []
+
+    def thunk(user, inp, nbytes, out):
+        try:
+            data = ag(inp, nbytes)
+            C.memmove(out, data, len(data))
+            return 0
+        except Exception as e:  # reported as KNNG_EWORLD by the library
+            err.append(e)
+            return 1
+    cb = _ALLGATHER_FN(thunk)
+    ds = _dataset(x)
+    res = _DistResult()
+    cc = cfg._c()
+    rows = _u64(0)
+    dev = device if device is not None else _device_of(x)
+    rc = lib().knng_build_distributed_rank(context().h, dev, rank, world_size, cb, None,
+                                           C.byref(ds), C.byref(cc), _ptr(out_i), _ptr(out_d),
+                                           _ptr(out_r), _mem(x), C.byref(rows), C.byref(res))
+    if rc != 0 and err:
+        raise WorldError(f"host transport failed: {err[0]!r}")
+    _check(rc)
+    m = rows.value
+    r = _dist_result(KnnGraph(out_i[:m], out_d[:m]), res)
+    return RankBuildResult(**{f.name: getattr(r, f.name) for f in dataclasses.fields(r)},
+                           rows=out_r[:m])
 
 
 def refine(x_perm, cfg: RefineConfig, offsets, ids, dists, mode: int = 0) -> DistBuildResult:

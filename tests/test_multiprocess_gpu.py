@@ -1,0 +1,67 @@
+"""One process per GPU rank (knng_build_distributed_rank): ranks exchange CUDA
+IPC handles of their published regions over a torch.distributed gloo group
+and pull one-sidedly.  The GPU NN-Descent is deterministic, so every rank's
+rows must equal the single-process build_distributed output bit for bit
+(refine.cpp:504-586; the schedule and gets are the reference's)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_main(rank, world, port, n, d, out_dir):
+    import torch
+    import torch.distributed as dist
+    import paper_2605_27691_b200 as knng
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    dev = rank % torch.cuda.device_count()
+    x = torch.from_numpy(knng.gen_random_dataset(n, d, "clustered", 42, 16)).to(f"cuda:{dev}")
+    cfg = knng.RefineConfig(ranks=world, groups=2, k=16, seed=7,
+                            nn=knng.NnDescentParams(k=16, seed=3),
+                            search=knng.SearchParams(k_s=16, beam_width=64, num_entry_points=32,
+                                                     seed=5))
+    r = knng.build_distributed_rank(x, cfg, rank, world)
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=r.graph.ids.cpu().numpy(),
+             dists=r.graph.dists.cpu().numpy(), rows=r.rows.cpu().numpy(),
+             gets=np.array([[g.src, g.target, g.bytes, g.epoch] for g in r.comm_log], np.uint64))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_rank_processes_match_single_process(knng, tmp_path, world):
+    import torch.multiprocessing as mp
+    n, d = 12_000, 24
+    mp.start_processes(_rank_main, args=(world, _free_port(), n, d, str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    x = knng.gen_random_dataset(n, d, "clustered", 42, 16)
+    cfg = knng.RefineConfig(ranks=world, groups=2, k=16, seed=7,
+                            nn=knng.NnDescentParams(k=16, seed=3),
+                            search=knng.SearchParams(k_s=16, beam_width=64, num_entry_points=32,
+                                                     seed=5))
+    ref = knng.build_distributed(x, cfg)
+    seen = np.zeros(n, bool)
+    for rank in range(world):
+        z = np.load(tmp_path / f"rank{rank}.npz")
+        rows = z["rows"].astype(np.int64)
+        assert not seen[rows].any()
+        seen[rows] = True
+        assert np.array_equal(z["ids"], ref.graph.ids[rows])
+        assert np.array_equal(z["dists"].view(np.uint32), ref.graph.dists[rows].view(np.uint32))
+        # every rank reports the same, complete comm log: the reference's gets
+        got = sorted(map(tuple, z["gets"].tolist()))
+        want = sorted((g.src, g.target, g.bytes, g.epoch) for g in ref.comm_log)
+        assert got == want
+    assert seen.all()
