@@ -255,66 +255,72 @@ __device__ __forceinline__ u64 score_batch(const SearchArgs& a, const float* __r
   return take ? pack_key(__fsqrt_rn(acc), id) : kEmptyKey;
 }
 
-// Merge the lane-held candidate keys (kEmptyKey = none) into the beam.  A
-// candidate whose key is already in the beam (an id re-scored after it fell
-// out of the lossy visited filter: same id => same key) is dropped.
-__device__ __forceinline__ void beam_merge(u64 c, u64* __restrict__ s_beam, u32* __restrict__ s_exp,
-                                           u64* __restrict__ s_cand, int& cur, u32& bs, u32 width) {
+// Merge the lane-held candidate keys (kEmptyKey = none) into the sorted
+// beam in place: the beam becomes the top-`width` of (beam U candidates),
+// which is what the reference's sequential beam_insert leaves.  A candidate
+// whose key is already in the beam (an id re-scored after it fell out of the
+// lossy visited filter: same id => same key) is dropped.  No sort: with
+// clo = #beam < c, a kept candidate lands at clo + #kept < c and beam entry i
+// moves right by #{kept : clo <= i}.  Groups of 32 entries are rewritten from
+// the end (entries only move right, so every group is read before a write can
+// reach it); unmoved entries are not stored.
+__device__ __forceinline__ void beam_merge(u64 c, u64* __restrict__ beam,
+                                           unsigned char* __restrict__ flag,
+                                           u32* __restrict__ s_clo, u32& bs, u32 width) {
   const unsigned lane = lane_id();
-  if (bs == width && c != kEmptyKey && c >= s_beam[cur * width + width - 1]) c = kEmptyKey;
+  if (bs == width && c != kEmptyKey && c >= beam[width - 1]) c = kEmptyKey;
   if (!__any_sync(kFull, c != kEmptyKey)) return;
-  c = warp_sort32(c);
-  const u32 nc0 = __popc(__ballot_sync(kFull, c != kEmptyKey));
-  const int nxt = cur ^ 1;
-  u64* dst = s_beam + nxt * width;
-  u32* dexp = s_exp + nxt * 32;
-  const u64* src = s_beam + cur * width;
-  const u32* sexp = s_exp + cur * 32;
-  // candidates: rank among the beam (# beam < c), duplicate test
   u32 clo = 0;
   bool keep = false;
-  if (lane < nc0) {
+  if (c != kEmptyKey) {
     u32 hi = bs;
     while (clo < hi) {
       const u32 mid = (clo + hi) >> 1;
-      if (src[mid] < c) clo = mid + 1; else hi = mid;
+      if (beam[mid] < c) clo = mid + 1; else hi = mid;
     }
-    keep = !(clo < bs && src[clo] == c);
+    keep = !(clo < bs && beam[clo] == c);
   }
   const unsigned kb = __ballot_sync(kFull, keep);
   if (!kb) return;
   const u32 nc = __popc(kb);
-  const u32 ci = __popc(kb & lanemask_lt());
-  if (keep) s_cand[ci] = c;
-  const u32 words = (width + 31) >> 5;
-  if (lane < words) dexp[lane] = 0;
-  __syncwarp();
-  // beam entries: new position = i + #cands < b
-  for (u32 i = lane; i < bs; i += 32) {
-    const u64 b = src[i];
-    u32 lo = 0, hi = nc;
-    while (lo < hi) {
-      const u32 mid = (lo + hi) >> 1;
-      if (s_cand[mid] < b) lo = mid + 1; else hi = mid;
-    }
-    const u32 pos = i + lo;
-    if (pos < width) {
-      dst[pos] = b;
-      if ((sexp[i >> 5] >> (i & 31)) & 1u) atomicOr(&dexp[pos >> 5], 1u << (pos & 31));
-    }
+  // rank among the kept candidates (keys are distinct)
+  u32 crank = 0;
+  for (unsigned m = kb; m;) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    const u64 cj = __shfl_sync(kFull, c, j);
+    crank += (keep && cj < c) ? 1u : 0u;
   }
-  // candidates: new position = j + #beam < c
-  if (keep) {
-    const u32 pos = ci + clo;
-    if (pos < width) dst[pos] = c;
+  if (keep) s_clo[__popc(kb & lanemask_lt())] = clo;
+  __syncwarp();
+  for (int t = (int)((bs + 31) >> 5) - 1; t >= 0; --t) {
+    const u32 i = lane + 32u * (u32)t;
+    const bool valid = i < bs;
+    u64 b = 0;
+    unsigned char f = 0;
+    u32 sh = 0;
+    if (valid) {
+      b = beam[i];
+      f = flag[i];
+      for (u32 j = 0; j < nc; ++j) sh += s_clo[j] <= i ? 1u : 0u;
+    }
+    __syncwarp();
+    if (valid && sh && i + sh < width) {
+      beam[i + sh] = b;
+      flag[i + sh] = f;
+    }
+    __syncwarp();
+  }
+  if (keep && clo + crank < width) {
+    beam[clo + crank] = c;
+    flag[clo + crank] = 0;
   }
   __syncwarp();
-  cur = nxt;
   bs = min(width, bs + nc);
 }
 
 struct SmemLayout {
-  size_t q, vis, beam, cand, exp, stage, ptr, total;
+  size_t q, vis, beam, flag, clo, stage, ptr, total;
 };
 
 __host__ __device__ inline SmemLayout search_layout(int d, u32 width, u32 vis_slots, u32 stride) {
@@ -325,15 +331,15 @@ __host__ __device__ inline SmemLayout search_layout(int d, u32 width, u32 vis_sl
   L.stage = off;
   off += (size_t)32 * stride * 4;
   L.beam = off;
-  off += (size_t)2 * width * 8;
-  L.cand = off;
-  off += 32 * 8;
+  off += (size_t)width * 8;
   L.ptr = off;
   off += 32 * 8;
+  L.clo = off;
+  off += 32 * 4;
   L.vis = off;
   off += (size_t)vis_slots * 4;
-  L.exp = off;
-  off += 2 * 32 * 4;
+  L.flag = off;
+  off += ((size_t)width + 15) & ~size_t(15);
   L.total = off;
   return L;
 }
@@ -349,10 +355,10 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
   float* s_q = reinterpret_cast<float*>(smem + L.q);
   float* s_stage = reinterpret_cast<float*>(smem + L.stage);
   u64* s_beam = reinterpret_cast<u64*>(smem + L.beam);
-  u64* s_cand = reinterpret_cast<u64*>(smem + L.cand);
+  unsigned char* s_flag = smem + L.flag;  // 1 = expanded (BeamEntry::expanded)
+  u32* s_clo = reinterpret_cast<u32*>(smem + L.clo);
   u64* s_ptr = reinterpret_cast<u64*>(smem + L.ptr);
   u32* s_vis = reinterpret_cast<u32*>(smem + L.vis);
-  u32* s_exp = reinterpret_cast<u32*>(smem + L.exp);
 
   u64 tot_hops = 0, tot_scored = 0, tot_ovf = 0;
   for (u64 q = blockIdx.x; q < a.nq; q += gridDim.x) {
@@ -363,7 +369,6 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
     __syncwarp();
     Visited vis{s_vis, a.vis_slots - 1, a.gtable ? a.gtable + (u64)blockIdx.x * a.gcap : nullptr,
                 a.gcap, (u32)(q + 1), false, 0};
-    int cur = 0;
     u32 bs = 0;
     u32 scored = 0;
 
@@ -378,7 +383,7 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
     };
     auto score_and_merge = [&](u32 id, bool take) {
       const u64 c = score_batch(a, s_q, s_stage, s_ptr, id, take);
-      beam_merge(c, s_beam, s_exp, s_cand, cur, bs, W);
+      beam_merge(c, s_beam, s_flag, s_clo, bs, W);
     };
 
     // entry points: sample_distinct(n, entries, Rng(mix_seed(seed, 0xa11ce000+q)))
@@ -414,25 +419,25 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
         score_and_merge(x, take);
       }
     }
-    if (a.cache) vis.to_filter(s_beam + cur * W, bs);
+    if (a.cache) vis.to_filter(s_beam, bs);
 
     // expansion loop (annsearch.cpp:103-120)
     u32 hops = 0;
     while (hops < a.max_hops) {
-      const u32 words = (bs + 31) >> 5;
-      u32 w = 0;
-      if (lane < words) {
-        const u32 valid = (lane == words - 1 && (bs & 31)) ? ((1u << (bs & 31)) - 1u) : kFull;
-        w = ~s_exp[cur * 32 + lane] & valid;
+      // first unexpanded beam entry (annsearch.cpp:104-108)
+      u32 idx = kNoId;
+      for (u32 t = 0; t * 32 < bs; ++t) {
+        const u32 i = t * 32 + lane;
+        const unsigned m = __ballot_sync(kFull, i < bs && s_flag[i] == 0);
+        if (m) {
+          idx = t * 32 + (__ffs(m) - 1);
+          break;
+        }
       }
-      const unsigned nz = __ballot_sync(kFull, w != 0);
-      if (!nz) break;  // every beam entry expanded
-      const int wl = __ffs(nz) - 1;
-      const u32 wv = __shfl_sync(kFull, w, wl);
-      const u32 idx = (u32)wl * 32 + (__ffs(wv) - 1);
-      const u32 u = key_id(s_beam[cur * W + idx]);
+      if (idx == kNoId) break;  // every beam entry expanded
+      const u32 u = key_id(s_beam[idx]);
       __syncwarp();
-      if (lane == 0) s_exp[cur * 32 + (idx >> 5)] |= 1u << (idx & 31);
+      if (lane == 0) s_flag[idx] = 1;
       __syncwarp();
       for (u32 c0 = 0; c0 < a.deg; c0 += 32) {
         const u32 nb = (c0 + lane < a.deg) ? __ldg(a.sg + (u64)u * a.deg + c0 + lane) : kNoId;
@@ -456,7 +461,7 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
       u32 id = 0;
       float dd = 0.0f;
       if (i < bs) {
-        const u64 key = s_beam[cur * W + i];
+        const u64 key = s_beam[i];
         id = key_id(key) + a.id_base;
         dd = key_dist(key);
       }
