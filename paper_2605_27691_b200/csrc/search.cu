@@ -211,11 +211,24 @@ __device__ __forceinline__ u64 score_batch(const SearchArgs& a, const float* __r
       const u32 sbase = (u32)__cvta_generic_to_shared(stage) + sub * 16;
       const uintptr_t gofs = (uintptr_t)(c0 + sub * 4) * 4;
       if (sub * 4 < cl) {
-        for (u32 k = g; k < nf; k += rpi) {
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + k * a.stride * 4),
-                       "l"((uintptr_t)s_ptr[k] + gofs) : "memory");
-          for (u32 t = sub * 4 + 128; t < cl; t += 128)
-            cpa16(stage + k * a.stride + t, reinterpret_cast<const float*>((uintptr_t)s_ptr[k]) + c0 + t);
+        // 4 rows per trip: back-to-back LDGSTS share the loop and the
+        // compiler's per-group LDGSTS padding
+        const u32 step = 4 * rpi;
+        for (u32 k = g; k < nf; k += step) {
+#pragma unroll
+          for (u32 j = 0; j < 4; ++j) {
+            const u32 kk = k + j * rpi;
+            if (kk < nf)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n"
+                           ::"r"(sbase + kk * a.stride * 4), "l"((uintptr_t)s_ptr[kk] + gofs)
+                           : "memory");
+          }
+        }
+        if (cl > 128) {
+          for (u32 k = g; k < nf; k += rpi)
+            for (u32 t = sub * 4 + 128; t < cl; t += 128)
+              cpa16(stage + k * a.stride + t,
+                    reinterpret_cast<const float*>((uintptr_t)s_ptr[k]) + c0 + t);
         }
       }
     } else {
