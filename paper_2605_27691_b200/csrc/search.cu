@@ -305,8 +305,10 @@ __device__ __forceinline__ void beam_merge(u64 c, u64* __restrict__ beam,
     crank += (keep && cj < c) ? 1u : 0u;
   }
   if (keep) s_clo[__popc(kb & lanemask_lt())] = clo;
+  // entries before the first insertion point keep their slots
+  const u32 first = __reduce_min_sync(kFull, keep ? clo : 0xffffffffu);
   __syncwarp();
-  for (int t = (int)((bs + 31) >> 5) - 1; t >= 0; --t) {
+  for (int t = (int)((bs + 31) >> 5) - 1; t >= (int)(first >> 5); --t) {
     const u32 i = lane + 32u * (u32)t;
     const bool valid = i < bs;
     u64 b = 0;

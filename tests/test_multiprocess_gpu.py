@@ -40,7 +40,7 @@ def _rank_main(rank, world, port, n, d, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_rank_processes_match_single_process(knng, tmp_path, world):
     import torch.multiprocessing as mp
     n, d = 12_000, 24
