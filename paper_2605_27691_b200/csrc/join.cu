@@ -257,7 +257,7 @@ struct Smem {
   __device__ u32* pid(int m) const {
     return reinterpret_cast<u32*>(meta + m * meta_bytes + G * RMAX * 8 + G * 4);
   }
-  __device__ int* mhdr(int m) const {  // [0] chunk, [1] np
+  __device__ int* mhdr(int m) const {  // [0] chunk, [1] np, [2] offers queued
     return reinterpret_cast<int*>(meta + m * meta_bytes + G * RMAX * 8 + G * 8);
   }
   __device__ int* rb(int q) const { return reinterpret_cast<int*>(desc + q * desc_bytes); }
@@ -320,6 +320,7 @@ __device__ bool load_chunk(const JoinArgs& a, const Smem& s, int m) {
   if (tid == 0) {
     s.mhdr(m)[0] = (int)chunk;
     s.mhdr(m)[1] = np;
+    s.mhdr(m)[2] = 0;  // offers queued for this chunk (shared atomic)
   }
   __syncthreads();
   return true;
@@ -462,7 +463,7 @@ __global__ __launch_bounds__(kJT, 1) void k_join(JoinArgs a) {
   const int tid = threadIdx.x;
   const unsigned lane = lane_id(), warp = tid >> 5;
   u64 my_pairs = 0, my_rows = 0, my_offers = 0;
-  u32 q_used0 = 0, q_used1 = 0;  // offers queued per meta slot (uniform)
+  int pend_chunk = -1, pend_m = 0;  // chunk completed by the last batch (uniform)
 
   // prologue: first chunk, first batch, first dim chunk
   if (!load_chunk(a, s, 0)) return;
@@ -487,7 +488,6 @@ __global__ __launch_bounds__(kJT, 1) void k_join(JoinArgs a) {
       if (jn < s.mhdr(m)[1]) {
         form_batch(a, s, nq, m, jn, tn);
       } else if (load_chunk(a, s, m ^ 1)) {
-        if (m ^ 1) q_used1 = 0; else q_used0 = 0;
         form_batch(a, s, nq, m ^ 1, 0, 0);
       } else {
         have_next = false;
@@ -588,61 +588,74 @@ __global__ __launch_bounds__(kJT, 1) void k_join(JoinArgs a) {
         }
         my_q += __popc(pass_mask[t]);
       }
-      int incl = my_q;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(kFull, incl, o);
-        if ((int)lane >= o) incl += y;
-      }
-      if (lane == 31) s.misc[warp] = incl;
-      __syncthreads();
-      int wbase = 0, btot = 0;
-#pragma unroll
-      for (int w = 0; w < kJT / 32; ++w) {
-        if (w < (int)warp) wbase += s.misc[w];
-        btot += s.misc[w];
-      }
+      // queue order is irrelevant (bucket inserts are order-independent):
+      // each warp reserves one run of slots with a shared atomic, then every
+      // (pair, direction) bit position is written by one ballot -- the
+      // passing lanes store to consecutive slots (coalesced, branch-free)
       const u32 chunk = (u32)s.mhdr(m)[0];
       u64* qk = a.q_key + (u64)chunk * a.q_per_chunk;
       u32* qt = a.q_tgt + (u64)chunk * a.q_per_chunk;
-      const u32 qu = m ? q_used1 : q_used0;
-      u64 slot = qu + wbase + incl - my_q;
-      if (m) q_used1 += btot; else q_used0 += btot;
+      const int wq = __reduce_add_sync(kFull, (unsigned)my_q);
+      u32 wbase = 0;
+      if (lane == 0 && wq) wbase = (u32)atomicAdd(&s.mhdr(m)[2], wq);
+      u32 slot = __shfl_sync(kFull, wbase, 0);
 #pragma unroll
       for (int t = 0; t < kTPT; ++t) {
         const u32 pm = pass_mask[t];
-        if (!pm) continue;
+        if (!__any_sync(kFull, pm != 0)) continue;
         const int lb = T[t].pt * a.RMAX;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const u32 two = (pm >> ((r * 4 + c) * 2)) & 3u;
-            if (!two) continue;
+        for (int rc = 0; rc < 16; ++rc) {
+          const u32 two = (pm >> (rc * 2)) & 3u;
+          if (!__any_sync(kFull, two != 0)) continue;
+          const int r = rc >> 2, c = rc & 3;
+          u32 u = 0, v = 0;
+          float dist = 0.0f;
+          if (two) {
             const int i = T[t].ti + T[t].rstr * r;
             const int jj = T[t].tj + T[t].cstr * c;
-            const u32 u = s.ids(m)[lb + i], v = s.ids(m)[lb + (T[t].tri ? jj : T[t].nn + jj)];
-            const float dist = acc[t][r][c];
+            u = s.ids(m)[lb + i];
+            v = s.ids(m)[lb + (T[t].tri ? jj : T[t].nn + jj)];
+            dist = acc[t][r][c];
+          }
 #pragma unroll
-            for (int dir = 0; dir < 2; ++dir) {
-              if (!((two >> dir) & 1u)) continue;
-              qk[slot] = pack_key(dist, dir ? u : v);
-              qt[slot] = dir ? v : u;
-              ++slot;
+          for (int dir = 0; dir < 2; ++dir) {
+            const bool on = (two >> dir) & 1u;
+            const unsigned mb = __ballot_sync(kFull, on);
+            if (on) {
+              const u32 at = slot + __popc(mb & lanemask_lt());
+              qk[at] = pack_key(dist, dir ? u : v);
+              qt[at] = dir ? v : u;
             }
+            slot += __popc(mb);
           }
         }
       }
-      if (s.dhdr(cq)[4] >= s.mhdr(m)[1] && tid == 0) {  // chunk complete
-        a.q_fill[chunk] = qu + btot;
-        my_offers += qu + btot;
+      if (s.dhdr(cq)[4] >= s.mhdr(m)[1]) {  // chunk complete: fill after the barrier
+        pend_chunk = (int)chunk;
+        pend_m = m;
       }
     }
     if (!have_next) break;
     __syncthreads();  // everyone is done with buffer cbuf / desc slot before reuse
+    if (pend_chunk >= 0) {
+      // slot pend_m is reloaded only two chunks later: its counter is final
+      if (tid == 0) {
+        const u32 f = (u32)s.mhdr(pend_m)[2];
+        a.q_fill[pend_chunk] = f;
+        my_offers += f;
+      }
+      pend_chunk = -1;
+    }
     cq = nq;
     cc0 = nc0;
     cbuf = nbuf;
+  }
+  __syncthreads();
+  if (pend_chunk >= 0 && tid == 0) {
+    const u32 f = (u32)s.mhdr(pend_m)[2];
+    a.q_fill[pend_chunk] = f;
+    my_offers += f;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) my_pairs += __shfl_xor_sync(kFull, my_pairs, o);
