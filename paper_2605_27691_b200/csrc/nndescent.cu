@@ -43,6 +43,33 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// sample_distinct(bound, B, rng) rng.hpp:66-87 with the whole warp: the rng
+// stream is counter-addressed (draw m = sm64_draw(s, m)), so lane l evaluates
+// draw m0 + l; first occurrences that are not yet picked are taken in draw
+// order until B are picked -- the same picks, in the same order, as the serial
+// loop.  s_pick[i] (warp scratch) receives pick i; returns the draws consumed
+// (the serial loop's rng position afterwards).  Needs B <= 32 and B < bound.
+__device__ u32 warp_sample_distinct(u64 s, u64 m0, u64 bound, u32 B, u32* s_pick) {
+  const unsigned lane = lane_id();
+  u32 got = 0;
+  u64 m = m0;
+  while (true) {
+    const u32 x = (u32)__umul64hi(sm64_draw(s, m + lane), bound);
+    const unsigned grp = __match_any_sync(kFull, x);
+    bool fresh = (__ffs(grp) - 1) == (int)lane;  // first occurrence in this batch
+    for (u32 j = 0; j < got; ++j) fresh = fresh && s_pick[j] != x;
+    const unsigned fb = __ballot_sync(kFull, fresh);
+    const u32 before = __popc(fb & lanemask_lt());
+    const bool take = fresh && got + before < B;
+    if (take) s_pick[got + before] = x;
+    const unsigned last = __ballot_sync(kFull, take && got + before == B - 1);
+    __syncwarp();
+    if (last) return (u32)(m - m0) + (u32)__ffs(last);
+    got += __popc(fb);
+    m += 32;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // init_random_graph nndescent.cpp:29-62 -- warp per row
 // ---------------------------------------------------------------------------
@@ -86,6 +113,7 @@ __global__ __launch_bounds__(256) void k_sample_fwd(const u64* __restrict__ keys
                                                     u32* __restrict__ ofn,
                                                     u32* __restrict__ cnt_new,
                                                     u32* __restrict__ cnt_old, bool count_old) {
+  __shared__ u32 s_scr[8][64];  // per warp: picks | rank -> lane
   const unsigned lane = lane_id();
   const u32 km = kmask_of(k);
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
@@ -110,33 +138,26 @@ __global__ __launch_bounds__(256) void k_sample_fwd(const u64* __restrict__ keys
         flags[p] = 0;
       }
     } else {
-      // sample_distinct(np, B, Rng(mix_seed(iter_seed, p))) rng.hpp:66-87
-      Rng rng(mix_seed(iter_seed, p));
-      u32 picked = 0, my_pick = kNone;
-      for (u32 cnt = 0; cnt < B;) {
-        const u32 x = (u32)rng.next_below(np);
-        if ((picked >> x) & 1u) continue;
-        picked |= 1u << x;
-        if (lane == cnt) my_pick = x;
-        ++cnt;
+      // sample_distinct(np, B, Rng(mix_seed(iter_seed, p))) rng.hpp:66-87:
+      // pick i = the rank (among the new entries) of the i-th sampled one
+      u32* sp = s_scr[threadIdx.x >> 5];
+      u32* sr = sp + 32;
+      if (isnew) sr[__popc(fm & lt)] = lane;  // rank -> lane
+      warp_sample_distinct(mix_seed(iter_seed, p), 0, np, B, sp);
+      u32 src = 0;
+      if (lane < B) src = sr[sp[lane]];
+      const u32 idv = __shfl_sync(kFull, id, src);
+      if (lane < B) {
+        nf[p * B + lane] = idv;
+        atomicAdd(&cnt_new[idv], 1u);
       }
-      const u32 rank = isnew ? __popc(fm & lt) : kNone;
-      u32 cleared = 0;
-      for (u32 i = 0; i < B; ++i) {
-        const u32 pi = __shfl_sync(kFull, my_pick, i);
-        const unsigned b = __ballot_sync(kFull, rank == pi);
-        const int src = __ffs(b) - 1;
-        if ((int)lane == src) {
-          nf[p * B + i] = id;
-          atomicAdd(&cnt_new[id], 1u);
-        }
-        cleared |= b;
-      }
+      const u32 cleared = __reduce_or_sync(kFull, lane < B ? (1u << src) : 0u);
       if (lane == 0) {
         nfn[p] = B;
         ofn[p] = k - np;
         flags[p] = fm & ~cleared;
       }
+      __syncwarp();
     }
   }
 }
@@ -215,10 +236,13 @@ __global__ __launch_bounds__(256) void k_rev_select(u64 n, u32 B, u64 iter_seed,
                                                     u32* __restrict__ nr, u32* __restrict__ nrn,
                                                     u32* __restrict__ orv,
                                                     u32* __restrict__ orn) {
+  __shared__ u32 s_scr[8][32];  // per warp: picks
   const unsigned lane = lane_id();
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
   for (u64 v = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); v < n; v += warps) {
-    Rng rng(mix_seed(iter_seed, 0x8000000000000000ull | v));
+    const u64 rs = mix_seed(iter_seed, 0x8000000000000000ull | v);
+    u64 drawn = 0;  // rng position, shared by new_rev then old_rev
+    u32* sp = s_scr[threadIdx.x >> 5];
     for (int which = 0; which < 2; ++which) {
       const u64* off = which ? off_old : off_new;
       const u32* buf = which ? buf_old : buf_new;
@@ -233,15 +257,10 @@ __global__ __launch_bounds__(256) void k_rev_select(u64 n, u32 B, u64 iter_seed,
         continue;
       }
       // sample_distinct(len, B, rng) rng.hpp:66-87 over the sorted segment
-      u32 my_pick = kNone;
-      for (u32 cnt = 0; cnt < B;) {
-        const u32 x = (u32)rng.next_below(len);
-        if (__ballot_sync(kFull, lane < cnt && my_pick == x)) continue;
-        if (lane == cnt) my_pick = x;
-        ++cnt;
-      }
-      if (lane < B) out[lane] = seg[my_pick];
+      drawn += warp_sample_distinct(rs, drawn, len, B, sp);
+      if (lane < B) out[lane] = seg[sp[lane]];
       if (lane == 0) outn[v] = B;
+      __syncwarp();
     }
   }
 }
