@@ -73,26 +73,62 @@ __device__ u32 warp_sample_distinct(u64 s, u64 m0, u64 bound, u32 B, u32* s_pick
 // ---------------------------------------------------------------------------
 // init_random_graph nndescent.cpp:29-62 -- warp per row
 // ---------------------------------------------------------------------------
-__global__ __launch_bounds__(256) void k_init(const float* __restrict__ X, u64 n, int d, u32 k,
+constexpr u32 kInitDims = 64;  // dims per staging round (d % 4 == 0 path)
+
+constexpr int kInitThreads = 128;  // 4 warps: 4 x 8.7 KB staging fits static smem
+
+__global__ __launch_bounds__(kInitThreads) void k_init(const float* __restrict__ X, u64 n, int d, u32 k,
                                               u64 seed, u64* __restrict__ keys,
                                               u32* __restrict__ flags,
                                               float* __restrict__ worst) {
-  const unsigned lane = lane_id();
+  // per warp: 32 staged rows x (kInitDims + 4) floats | 32 picks
+  __shared__ __align__(16) float s_rows[kInitThreads / 32][32 * (kInitDims + 4)];
+  __shared__ u32 s_pick[kInitThreads / 32][32];
+  const unsigned lane = lane_id(), w = threadIdx.x >> 5;
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
-  for (u64 r = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
-    Rng rng(mix_seed(seed, r));
+  const bool vec = (d % 4) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  constexpr u32 kStride = kInitDims + 4;  // stride/4 odd: conflict-free LDS.128 by row
+  for (u64 r = (((u64)blockIdx.x * blockDim.x) >> 5) + w; r < n; r += warps) {
+    // k distinct non-self ids: sample_distinct(n - 1, k) in draw order, then
+    // the reference's skip-self shift (x >= r -> x + 1)
+    warp_sample_distinct(mix_seed(seed, r), 0, n - 1, k, s_pick[w]);
     u32 my_id = kNone;
-    u32 fill = 0;
-    while (fill < k) {
-      u32 id = (u32)rng.next_below(n - 1);
-      if (id >= r) ++id;
-      const bool dup = __ballot_sync(kFull, lane < fill && my_id == id) != 0;
-      if (dup) continue;
-      if (lane == fill) my_id = id;
-      ++fill;
+    if (lane < k) {
+      my_id = s_pick[w][lane];
+      if (my_id >= r) ++my_id;
+    }
+    const float* xr = X + r * (u64)d;
+    float acc = 0.0f;
+    if (vec) {
+      // stage the k neighbor rows chunk by chunk (coalesced cp.async, one
+      // 16-byte piece per lane, 2 rows per warp instruction at 64 dims) and
+      // sum each lane's own row in the reference's order
+      float* st = s_rows[w];
+      for (int c0 = 0; c0 < d; c0 += kInitDims) {
+        const int cl = min((int)kInitDims, d - c0);
+        const u32 pieces = (u32)cl / 4;          // 16-byte pieces per row
+        for (u32 e0 = 0; e0 < k * pieces; e0 += 32) {  // warp-uniform trips
+          const u32 e = e0 + lane;
+          const u32 j = e / pieces, q = e - j * pieces;
+          const u32 idj = __shfl_sync(kFull, my_id, j < 32 ? j : 0);
+          if (e < k * pieces) cp_async16(st + j * kStride + q * 4, X + (u64)idj * d + c0 + q * 4);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        if (lane < k) {
+          const float* my = st + lane * kStride;
+          for (int i = 0; i < cl; i += 4)
+            acc = sq_step4(acc, *reinterpret_cast<const float4*>(xr + c0 + i),
+                           *reinterpret_cast<const float4*>(my + i));
+        }
+        __syncwarp();
+      }
+    } else if (lane < k) {
+      const float* xo = X + (u64)my_id * d;
+      for (int i = 0; i < d; ++i) acc = sq_step(acc, xr[i], xo[i]);
     }
     u64 key = kEmptyKey;
-    if (lane < k) key = pack_key(l2_exact(X + r * d, X + (u64)my_id * d, d), my_id);
+    if (lane < k) key = pack_key(__fsqrt_rn(acc), my_id);
     key = warp_sort32(key);
     if (lane < k) keys[r * k + lane] = key;
     const u64 last = __shfl_sync(kFull, key, k - 1);
@@ -100,6 +136,7 @@ __global__ __launch_bounds__(256) void k_init(const float* __restrict__ X, u64 n
       flags[r] = kmask_of(k);
       worst[r] = key_dist(last);
     }
+    __syncwarp();
   }
 }
 
@@ -394,7 +431,8 @@ void init_random_graph_device(Runner& r, const DevRows& ds, uint32_t k, uint64_t
   require(k >= 1 && k < ds.n, "init_random_graph: need 1 <= k < N");
   require(k <= 32, "init_random_graph: the B200 path supports k <= 32");
   DBuf<float> worst(r, ds.n);
-  k_init<<<warp_grid(r, ds.n), 256, 0, r.stream>>>(ds.x, ds.n, ds.d, k, seed, keys, flags,
+  k_init<<<(unsigned)std::min<u64>(ceil_div<u64>(ds.n, kInitThreads / 32), (u64)r.num_sms * 32),
+           kInitThreads, 0, r.stream>>>(ds.x, ds.n, ds.d, k, seed, keys, flags,
                                                    worst.p);
   KNNG_LAUNCH_CHECK();
 }
@@ -516,7 +554,8 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   alloc_lists(r, n, k, B, s, c);
   uint64_t launches = 0;
 
-  k_init<<<warp_grid(r, n), 256, 0, r.stream>>>(ds.x, n, ds.d, k, p.seed, keys, flags, worst.p);
+  k_init<<<(unsigned)std::min<u64>(ceil_div<u64>(n, kInitThreads / 32), (u64)r.num_sms * 32),
+           kInitThreads, 0, r.stream>>>(ds.x, n, ds.d, k, p.seed, keys, flags, worst.p);
   KNNG_LAUNCH_CHECK();
   ++launches;
   tm.tick(kStInit);
