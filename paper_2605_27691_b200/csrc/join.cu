@@ -25,7 +25,14 @@ namespace knng_b200 {
 namespace {
 
 constexpr u32 kNone = 0xffffffffu;
-constexpr int kJT = 512;                // threads per join CTA
+#ifndef KNNG_JOIN_THREADS
+#define KNNG_JOIN_THREADS 256
+#endif
+#ifndef KNNG_JOIN_CTAS
+#define KNNG_JOIN_CTAS 2
+#endif
+constexpr int kJT = KNNG_JOIN_THREADS;  // threads per join CTA
+constexpr int kJCtas = KNNG_JOIN_CTAS;  // resident join CTAs per SM (latency overlap)
 constexpr int kTPT = 1;                 // micro-tiles per thread
 constexpr int kMaxTiles = kJT * kTPT;   // tiles per batch
 constexpr int G = kJoinChunk;
@@ -457,7 +464,7 @@ __device__ __forceinline__ Tile decode_tile(const Smem& s, int q, int t) {
   return T;
 }
 
-__global__ __launch_bounds__(kJT, 1) void k_join(JoinArgs a) {
+__global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Smem s = carve(smem, a.RMAX, a.RB, a.DCP);
   const int tid = threadIdx.x;
@@ -698,6 +705,10 @@ JoinPlan plan_join(const Runner& r, int d, uint32_t k, uint32_t B) {
   KNNG_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, r.device));
   // largest RB whose footprint fits (2 feature buffers + 2 row-id tables)
   int rb = 1024;
+  int smem_sm = 0;
+  KNNG_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, r.device));
+  // kJCtas CTAs must fit one SM (1 KB reserved per CTA)
+  smem_max = std::min(smem_max, smem_sm / kJCtas - 1024);
   while (rb > 0 && join_smem_bytes(p.RMAX, rb, p.DCP) + 1024 > (size_t)smem_max) rb -= 8;
   require(rb >= max_rows, "nn_descent: feature rows too wide for the join's smem batches");
   p.RB = rb;

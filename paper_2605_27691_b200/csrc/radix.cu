@@ -118,15 +118,15 @@ void sort_impl(const Runner& r, u32* keys, u32* vals, u32* tmp_keys, u32* tmp_va
   int passes = 0;
   for (u64 m = max_key; m; m >>= 8) ++passes;
   if (passes == 0) passes = 1;
-  DBuf<u32> hist(r, (u64)kDigits * ntiles);
-  DBuf<u64> base(r, (u64)kDigits * ntiles + 1);
+  u32* hist = static_cast<u32*>(r.scratch(Runner::kScrRadixHist, (u64)kDigits * ntiles * 4));
+  u64* base = static_cast<u64*>(r.scratch(Runner::kScrRadixBase, ((u64)kDigits * ntiles + 1) * 8));
   u32 *ik = keys, *iv = vals, *ok = tmp_keys, *ov = tmp_vals;
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
-    k_radix_count<<<(unsigned)ntiles, kRT, 0, r.stream>>>(ik, n, n_dev, shift, hist.p, ntiles);
+    k_radix_count<<<(unsigned)ntiles, kRT, 0, r.stream>>>(ik, n, n_dev, shift, hist, ntiles);
     KNNG_LAUNCH_CHECK();
-    exclusive_scan_u32(r, hist.p, base.p, (u64)kDigits * ntiles);
-    k_radix_scatter<<<(unsigned)ntiles, kRT, 0, r.stream>>>(ik, iv, n, n_dev, shift, base.p,
+    exclusive_scan_u32(r, hist, base, (u64)kDigits * ntiles);
+    k_radix_scatter<<<(unsigned)ntiles, kRT, 0, r.stream>>>(ik, iv, n, n_dev, shift, base,
                                                             ntiles, ok, ov);
     KNNG_LAUNCH_CHECK();
     std::swap(ik, ok);

@@ -95,18 +95,46 @@ struct Runner {
     stream = o.stream;
     num_sms = o.num_sms;
     owns = o.owns;
+    scratch_ = std::move(o.scratch_);
+    o.scratch_.clear();
     o.owns = false;
     o.stream = nullptr;
     return *this;
   }
   ~Runner() {
-    if (owns && stream) {
+    if (stream) {
       cudaSetDevice(device);
+      for (auto& sc : scratch_)
+        if (sc.first) cudaFreeAsync(sc.first, stream);
+    }
+    if (owns && stream) {
       cudaStreamSynchronize(stream);
       cudaStreamDestroy(stream);
     }
   }
   void sync() const { KNNG_CUDA(cudaStreamSynchronize(stream)); }
+
+  // Grow-only stream-ordered scratch, one buffer per slot (kernels on this
+  // stream that use a slot are ordered, so consecutive users share it).
+  // Per-iteration temporaries come from here: allocating and freeing them
+  // every iteration occasionally made the host wait on pool growth while
+  // the GPU idled (up to ~55 ms, seen with KNNG_TRACE_SLOW).
+  enum ScratchSlot { kScrScan = 0, kScrRadixHist, kScrRadixBase, kScrCount };
+  void* scratch(int slot, size_t bytes) const {
+    if (scratch_.size() < (size_t)kScrCount) scratch_.resize(kScrCount, {nullptr, 0});
+    auto& sc = scratch_[slot];
+    if (sc.second < bytes) {
+      DeviceGuard g(device);
+      if (sc.first) cudaFreeAsync(sc.first, stream);
+      const size_t cap = bytes + bytes / 4 + 256;
+      KNNG_CUDA(cudaMallocAsync(&sc.first, cap, stream));
+      sc.second = cap;
+    }
+    return sc.first;
+  }
+
+ private:
+  mutable std::vector<std::pair<void*, size_t>> scratch_;
 };
 
 // Stream-ordered device buffer.

@@ -89,12 +89,12 @@ void exclusive_scan_u32(const Runner& r, const uint32_t* in, uint64_t* out, uint
     return;
   }
   const u64 nb = ceil_div<u64>(n, kScanTile);
-  DBuf<u64> bsum(r, nb);
-  k_scan_tiles<<<(unsigned)nb, kScanThreads, 0, r.stream>>>(in, out, bsum.p, n);
+  u64* bsum = static_cast<u64*>(r.scratch(Runner::kScrScan, nb * sizeof(u64)));
+  k_scan_tiles<<<(unsigned)nb, kScanThreads, 0, r.stream>>>(in, out, bsum, n);
   KNNG_LAUNCH_CHECK();
-  k_scan_bsums<<<1, kScanThreads, 0, r.stream>>>(bsum.p, nb, out + n);
+  k_scan_bsums<<<1, kScanThreads, 0, r.stream>>>(bsum, nb, out + n);
   KNNG_LAUNCH_CHECK();
-  k_scan_add<<<(unsigned)ceil_div<u64>(n, 256), 256, 0, r.stream>>>(out, bsum.p, n);
+  k_scan_add<<<(unsigned)ceil_div<u64>(n, 256), 256, 0, r.stream>>>(out, bsum, n);
   KNNG_LAUNCH_CHECK();
 }
 
