@@ -127,7 +127,14 @@ __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
                                                const u32* __restrict__ q_tgt,
                                                const u32* __restrict__ q_fill, u64 q_per_chunk,
                                                u32 chunks, u64* __restrict__ slots, u32 S,
-                                               u32 nb, u32 ways, u64* __restrict__ counters) {
+                                               u32 nb, u32 ways, u64* __restrict__ counters,
+                                               u64 p_lo, const u64* __restrict__ n_live) {
+  if (n_live) {  // the slice's live chunk count, read on the device
+    const u64 live = *n_live;
+    const u64 hi = live < p_lo ? 0 : live - p_lo;
+    const u64 c = (hi + G - 1) / G;
+    if (c < chunks) chunks = (u32)c;
+  }
   for (u32 region = blockIdx.x; region < chunks; region += gridDim.x) {
     const u32 fill = q_fill[region];
     if (threadIdx.x == 0 && counters)
@@ -215,6 +222,7 @@ struct JoinArgs {
   const float* worst;
   const u32* act;  // active point list (null: points p_lo..p_hi themselves)
   u64 p_lo, p_hi;
+  const u64* n_live;  // device count bounding p_hi (null: none)
   u32* chunk_counter;
   u64* q_key;
   u32* q_tgt;
@@ -307,9 +315,14 @@ __device__ bool load_chunk(const JoinArgs& a, const Smem& s, int m) {
   if (tid == 0) s.misc[16] = (int)atomicAdd(a.chunk_counter, 1u);
   __syncthreads();
   const u32 chunk = (u32)s.misc[16];
+  u64 p_hi = a.p_hi;
+  if (a.n_live) {
+    const u64 live = *a.n_live;
+    if (live < p_hi) p_hi = live;
+  }
   const u64 p0 = a.p_lo + (u64)chunk * G;
-  if (p0 >= a.p_hi) return false;
-  const int np = (a.p_hi - p0) < (u64)G ? (int)(a.p_hi - p0) : G;
+  if (p0 >= p_hi) return false;
+  const int np = (p_hi - p0) < (u64)G ? (int)(p_hi - p0) : G;
   if (tid < np) {
     const u32 pt = a.act ? a.act[p0 + tid] : (u32)(p0 + tid);
     s.pid(m)[tid] = pt;
@@ -755,6 +768,7 @@ void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& l) {
   a.act = l.act;
   a.p_lo = l.p_lo;
   a.p_hi = l.p_hi;
+  a.n_live = l.n_live;
   a.chunk_counter = l.chunk_counter;
   a.q_key = l.q_key;
   a.q_tgt = l.q_tgt;
@@ -770,11 +784,12 @@ void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& l) {
 
 void launch_offer(const Runner& r, const JoinPlan& plan, const uint64_t* q_key,
                   const uint32_t* q_tgt, const uint32_t* q_fill, uint32_t chunks,
-                  uint64_t* slots, uint32_t S, uint32_t nb, uint32_t ways, uint64_t* counters) {
+                  uint64_t* slots, uint32_t S, uint32_t nb, uint32_t ways, uint64_t* counters,
+                  uint64_t p_lo, const uint64_t* n_live) {
   if (!chunks) return;
   const unsigned grid = (unsigned)std::min<uint64_t>(chunks, (uint64_t)r.num_sms * 8);
   k_offer<<<grid, 256, 0, r.stream>>>(q_key, q_tgt, q_fill, plan.q_per_chunk, chunks, slots, S,
-                                      nb, ways, counters);
+                                      nb, ways, counters, p_lo, n_live);
   KNNG_LAUNCH_CHECK();
 }
 

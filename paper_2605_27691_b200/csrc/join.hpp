@@ -39,6 +39,7 @@ struct JoinLaunch {
   const float* worst = nullptr;
   const uint32_t* act = nullptr;  // active point list; [p_lo, p_hi) index it (null: points)
   uint64_t p_lo = 0, p_hi = 0;
+  const uint64_t* n_live = nullptr;  // device count bounding p_hi (null: none)
   uint32_t* chunk_counter = nullptr;  // zeroed before each launch
   uint64_t* q_key = nullptr;
   uint32_t* q_tgt = nullptr;
@@ -57,6 +58,7 @@ void build_active_list(const Runner& r, uint64_t n, const uint32_t* L_cnt, uint3
 void launch_offer(const Runner& r, const JoinPlan& plan, const uint64_t* q_key,
                   const uint32_t* q_tgt, const uint32_t* q_fill, uint32_t chunks,
                   uint64_t* slots, uint32_t S, uint32_t nb, uint32_t ways,
-                  uint64_t* counters = nullptr);
+                  uint64_t* counters = nullptr, uint64_t p_lo = 0,
+                  const uint64_t* n_live = nullptr);
 
 }  // namespace knng_b200

@@ -565,10 +565,11 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   DBuf<u32> L_ids(r, n * plan.RMAX), L_cnt(r, n);
   // Offer queue: each point chunk owns a region sized for its worst case (2
   // offers per pair, max pairs C(2B,2) + 2B(k+B)), so nothing can overflow;
-  // points are processed in slices to bound the queue to ~4 GB.
+  // points are processed in slices to bound the queue (budget below).
   size_t free_b = 0, total_b = 0;
   KNNG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const u64 budget = std::min<u64>(4ull << 30, free_b / 4);
+  // 24 GB of worst-case queue (B200: 180 GB HBM): C2 runs in 2 slices
+  const u64 budget = std::min<u64>(24ull << 30, free_b / 4);
   u64 chunks_per_slice = std::max<u64>(1, budget / (plan.q_per_chunk * 12));
   u64 slice = chunks_per_slice * kJoinChunk;
   if (slice > n) {
@@ -607,21 +608,21 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
     tm.tick(kStLists);
     build_active_list(r, n, L_cnt.p, act_flag.p, act_off.p, act.p);
     launches += 5;
-    KNNG_CUDA(cudaMemcpyAsync(hcount.p + kCntActive, act_off.p + n, sizeof(u64),
-                              cudaMemcpyDeviceToHost, r.stream));
-    r.sync();
-    const u64 n_act = hcount.p[kCntActive];
-    const u64 nslices = ceil_div<u64>(n_act, slice);
+    // the active count stays on the device: every slice is launched and its
+    // kernels bound themselves by it (no host round trip mid-iteration; the
+    // slices past the count exit at once)
+    jl.n_live = act_off.p + n;
+    const u64 nslices = ceil_div<u64>(n, slice);
     for (u64 si = 0; si < nslices; ++si) {
       jl.p_lo = si * slice;
-      jl.p_hi = std::min<u64>(n_act, jl.p_lo + slice);
+      jl.p_hi = std::min<u64>(n, jl.p_lo + slice);
       chunk_ctr.zero();
       tm.tick(kStLists);
       launch_join(r, plan, jl);
       tm.tick(kStJoin);
       launch_offer(r, plan, q_key.p, q_tgt.p, q_fill.p,
                    (u32)ceil_div<u64>(jl.p_hi - jl.p_lo, (u64)kJoinChunk), slots.p, S, nb, ways,
-                   counters.p);
+                   counters.p, jl.p_lo, jl.n_live);
       tm.tick(kStOffer);
       launches += 2;
     }
