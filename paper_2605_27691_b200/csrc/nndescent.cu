@@ -568,8 +568,9 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   // points are processed in slices to bound the queue (budget below).
   size_t free_b = 0, total_b = 0;
   KNNG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  // 24 GB of worst-case queue (B200: 180 GB HBM): C2 runs in 2 slices
-  const u64 budget = std::min<u64>(24ull << 30, free_b / 4);
+  // up to 64 GB of worst-case queue (B200: 180 GB HBM): C2 runs as a single
+  // slice (one join + one offer launch per iteration)
+  const u64 budget = std::min<u64>(64ull << 30, free_b / 3);
   u64 chunks_per_slice = std::max<u64>(1, budget / (plan.q_per_chunk * 12));
   u64 slice = chunks_per_slice * kJoinChunk;
   if (slice > n) {
