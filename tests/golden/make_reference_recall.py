@@ -36,6 +36,7 @@ CONFIGS = {
     "c4r_100k_d96_clustered16_p2": (100_000, 96, "clustered", 16, 32, 2, 128, 96),
     "c4r_100k_d96_clustered16_p4": (100_000, 96, "clustered", 16, 32, 4, 128, 96),
     "c4r_100k_d96_clustered16_p8": (100_000, 96, "clustered", 16, 32, 8, 128, 96),
+    "c3_1m_d960_clustered1000_k32": (1_000_000, 960, "clustered", 1000, 32, 1, 64, 16),
     # bench.py --gpus N (weak scaling, C4 regime): N x 1M x 128 clustered(16), P=N, M=2
     "dist_p2_2m_clustered16_k32": (2_000_000, 128, "clustered", 16, 32, 2, 128, 96),
     "dist_p4_4m_clustered16_k32": (4_000_000, 128, "clustered", 16, 32, 4, 128, 96),
