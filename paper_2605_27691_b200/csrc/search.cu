@@ -211,18 +211,27 @@ __device__ __forceinline__ u64 score_batch(const SearchArgs& a, const float* __r
       const u32 sbase = (u32)__cvta_generic_to_shared(stage) + sub * 16;
       const uintptr_t gofs = (uintptr_t)(c0 + sub * 4) * 4;
       if (sub * 4 < cl) {
-        // 4 rows per trip: back-to-back LDGSTS share the loop and the
-        // compiler's per-group LDGSTS padding
+        // 4 rows per trip from one asm block (the copies stay back-to-back,
+        // so they share the compiler's LDGSTS padding); a trip's rows past nf
+        // copy a stale (valid) pointer into an unused slot instead of being
+        // predicated off
+        const u32 stride_b = a.stride * 4;
         const u32 step = 4 * rpi;
+        u32 dst = sbase + g * stride_b;
+        const u32 dstep = rpi * stride_b;
         for (u32 k = g; k < nf; k += step) {
-#pragma unroll
-          for (u32 j = 0; j < 4; ++j) {
-            const u32 kk = k + j * rpi;
-            if (kk < nf)
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n"
-                           ::"r"(sbase + kk * a.stride * 4), "l"((uintptr_t)s_ptr[kk] + gofs)
-                           : "memory");
-          }
+          const u32 k1 = min(k + rpi, 31u), k2 = min(k + 2 * rpi, 31u), k3 = min(k + 3 * rpi, 31u);
+          const uintptr_t s0 = (uintptr_t)s_ptr[k] + gofs, s1 = (uintptr_t)s_ptr[k1] + gofs;
+          const uintptr_t s2 = (uintptr_t)s_ptr[k2] + gofs, s3 = (uintptr_t)s_ptr[k3] + gofs;
+          asm volatile(
+              "cp.async.cg.shared.global [%0], [%1], 16;\n"
+              "cp.async.cg.shared.global [%2], [%3], 16;\n"
+              "cp.async.cg.shared.global [%4], [%5], 16;\n"
+              "cp.async.cg.shared.global [%6], [%7], 16;\n" ::"r"(dst), "l"(s0),
+              "r"(sbase + k1 * stride_b), "l"(s1), "r"(sbase + k2 * stride_b), "l"(s2),
+              "r"(sbase + k3 * stride_b), "l"(s3)
+              : "memory");
+          dst += 4 * dstep;
         }
         if (cl > 128) {
           for (u32 k = g; k < nf; k += rpi)
@@ -375,6 +384,9 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
   u64* s_ptr = reinterpret_cast<u64*>(smem + L.ptr);
   u32* s_vis = reinterpret_cast<u32*>(smem + L.vis);
 
+  // every staging slot pointer is always a valid row (see score_batch)
+  s_ptr[lane] = (u64)(uintptr_t)a.V;
+  __syncwarp();
   u64 tot_hops = 0, tot_scored = 0, tot_ovf = 0;
   for (u64 q = blockIdx.x; q < a.nq; q += gridDim.x) {
     // stage query, clear visited
