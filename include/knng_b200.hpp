@@ -407,6 +407,74 @@ inline DistBuildResult build_distributed(const Dataset& d, const RefineConfig& c
   return res;
 }
 
+// One rank of build_distributed in this process (one process per GPU; B200
+// extension, no reference counterpart).  `allgather(in, bytes, out)` must
+// gather `bytes` from every rank into `out` in rank order (MPI_Allgather,
+// torch.distributed, ...).  Returns this rank's rows (external ids) and, in
+// `rows`, the external id of each row.
+struct RankBuildResult {
+  KnnGraph graph;  // rows x k
+  std::vector<std::uint32_t> rows;
+  DistBuildResult::Phases phases;
+  std::vector<GetRecord> comm_log;  // every rank's gets
+};
+
+namespace detail {
+template <class F>
+int allgather_thunk(void* user, const void* in, std::uint64_t bytes, void* out) {
+  try {
+    (*static_cast<F*>(user))(in, static_cast<std::size_t>(bytes), out);
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+}  // namespace detail
+
+template <class AllGather>
+inline RankBuildResult build_distributed_rank(const Dataset& d, const RefineConfig& cfg,
+                                              std::size_t rank, std::size_t world, int device,
+                                              AllGather allgather) {
+  knng_refine_config c{};
+  c.ranks = world;
+  c.groups = cfg.groups;
+  c.k = cfg.k;
+  c.k_s = cfg.k_s;
+  c.out_degree = cfg.out_degree;
+  c.nn = knng_nnd_params{cfg.k, cfg.nn.delta, cfg.nn.rho, cfg.nn.max_iters,
+                         cfg.nn.candidate_capacity, cfg.nn.seed, cfg.nn.workers};
+  c.search = knng_search_params{cfg.search.k_s, cfg.search.beam_width, cfg.search.num_entry_points,
+                                cfg.search.max_hops, cfg.search.seed, cfg.search.workers};
+  c.skip_tree_phase = cfg.skip_tree_phase;
+  c.double_buffer = cfg.double_buffer;
+  c.max_concat_bytes = cfg.max_concat_bytes;
+  c.seed = cfg.seed;
+  const std::size_t cap = (d.num_points + world - 1) / world;
+  std::vector<std::uint32_t> ids(cap * cfg.k), rows(cap);
+  std::vector<float> dists(cap * cfg.k);
+  const knng_dataset ds = d.view();
+  knng_dist_result r{};
+  std::uint64_t n_rows = 0;
+  detail::check(knng_build_distributed_rank(detail::ctx(), device, rank, world,
+                                            &detail::allgather_thunk<AllGather>, &allgather, &ds,
+                                            &c, ids.data(), dists.data(), rows.data(),
+                                            KNNG_MEM_HOST, &n_rows, &r));
+  RankBuildResult res;
+  res.graph = KnnGraph::allocate(n_rows, cfg.k, IdSpace::global);
+  res.graph.flags.clear();
+  res.graph.ids.assign(ids.begin(), ids.begin() + n_rows * cfg.k);
+  res.graph.dists.assign(dists.begin(), dists.begin() + n_rows * cfg.k);
+  res.rows.assign(rows.begin(), rows.begin() + n_rows);
+  res.phases = {r.local_s, r.tree_s, r.merge_s, r.flat_s, r.etc_s};
+  std::vector<knng_get_record> recs(r.comm_gets ? r.comm_gets : 1);
+  std::uint64_t cnt = 0;
+  detail::check(knng_last_comm_log(detail::ctx(), recs.data(), recs.size(), &cnt));
+  for (std::uint64_t i = 0; i < cnt; ++i)
+    res.comm_log.push_back({recs[i].src, recs[i].target, recs[i].region, recs[i].bytes,
+                            recs[i].epoch});
+  return res;
+}
+
 // evalio.hpp (measurement support)
 enum class Distribution { uniform, gaussian, clustered };
 

@@ -4,6 +4,7 @@
 // reference test (file:line in the comment); prints PASS/FAIL per case and
 // exits non-zero on any failure.
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <filesystem>
 #include <functional>
@@ -104,6 +105,24 @@ int main() {
     p.seed = 2;
     const KnnGraph g = nn_descent(d, p);
     require(r.graph.ids == g.ids && r.graph.dists == g.dists, "P=1 differs from nn_descent");
+  });
+  run("one-rank build_distributed_rank == build_distributed P=1 (B200 per-process driver)", [] {
+    const Dataset d = gen_random_dataset(2000, 16, Distribution::clustered, 3, 10);
+    RefineConfig cfg;
+    cfg.ranks = 1;
+    cfg.k = 16;
+    cfg.nn.seed = 2;
+    const DistBuildResult full = build_distributed(d, cfg);
+    auto gather = [](const void* in, std::size_t n, void* out) { std::memcpy(out, in, n); };
+    const RankBuildResult r = build_distributed_rank(d, cfg, 0, 1, 0, gather);
+    require(r.rows.size() == d.num_points, "one rank owns every row");
+    bool same = true;
+    for (std::size_t i = 0; i < r.rows.size(); ++i)
+      for (std::size_t j = 0; j < cfg.k; ++j) {
+        same &= r.graph.ids[i * cfg.k + j] == full.graph.ids[r.rows[i] * cfg.k + j];
+        same &= r.graph.dists[i * cfg.k + j] == full.graph.dists[r.rows[i] * cfg.k + j];
+      }
+    require(same, "rank rows differ from build_distributed");
   });
   run("distributed P=4 quality + comm log (acceptance.cpp:72-103, 253-322)", [] {
     const Dataset d = gen_random_dataset(8000, 16, Distribution::clustered, 7100, 16);
