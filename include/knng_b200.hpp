@@ -407,6 +407,40 @@ inline DistBuildResult build_distributed(const Dataset& d, const RefineConfig& c
   return res;
 }
 
+// search_throughput_probe annsearch.cpp:131-155 (annsearch.hpp:52-69)
+struct ThroughputCase {
+  std::size_t source_count = 0;
+  const SearchGraph* sgraph = nullptr;
+  const Dataset* vectors = nullptr;
+};
+struct ThroughputRow {
+  std::size_t source_count = 0;
+  std::size_t num_queries = 0;
+  double seconds = 0.0;
+  double qps = 0.0;
+};
+inline std::vector<ThroughputRow> search_throughput_probe(const std::vector<ThroughputCase>& cases,
+                                                          const Dataset& queries,
+                                                          const SearchParams& params) {
+  std::vector<knng_dataset> vds(cases.size());
+  std::vector<knng_throughput_case> cc(cases.size());
+  for (std::size_t i = 0; i < cases.size(); ++i) {
+    vds[i] = cases[i].vectors->view();
+    cc[i] = knng_throughput_case{cases[i].source_count, cases[i].sgraph->ids.data(),
+                                 cases[i].sgraph->num_sources, cases[i].sgraph->out_degree, &vds[i],
+                                 KNNG_MEM_HOST};
+  }
+  const knng_dataset q = queries.view();
+  const knng_search_params p{params.k_s, params.beam_width, params.num_entry_points,
+                             params.max_hops, params.seed, params.workers};
+  std::vector<knng_throughput_row> rows(cases.size());
+  detail::check(knng_search_throughput_probe(detail::ctx(), 0, cc.data(), cc.size(), &q, &p,
+                                             rows.data()));
+  std::vector<ThroughputRow> out;
+  for (const auto& r : rows) out.push_back({r.source_count, r.num_queries, r.seconds, r.qps});
+  return out;
+}
+
 // One rank of build_distributed in this process (one process per GPU; B200
 // extension, no reference counterpart).  `allgather(in, bytes, out)` must
 // gather `bytes` from every rank into `out` in rank order (MPI_Allgather,

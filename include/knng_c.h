@@ -204,6 +204,28 @@ knng_status knng_ann_search(knng_ctx* ctx, int device, const knng_dataset* queri
                             uint8_t out_mem, uint32_t* out_ids, float* out_dists,
                             uint32_t* hops, uint32_t* scored);
 
+/* search_throughput_probe annsearch.cpp:131-155 (ThroughputCase / Row,
+ * annsearch.hpp:52-69): the batch search of `queries` against each case's
+ * graph, cases in ascending source_count; seconds = device time of the
+ * search (CUDA events on the context stream; inputs staged before timing).
+ * sg_ids host or device per sg_mem. */
+typedef struct {
+  uint64_t source_count;
+  const uint32_t* sg_ids;
+  uint64_t sg_n, degree;
+  const knng_dataset* vectors;
+  uint8_t sg_mem;
+} knng_throughput_case;
+typedef struct {
+  uint64_t source_count, num_queries;
+  double seconds, qps;
+} knng_throughput_row;
+knng_status knng_search_throughput_probe(knng_ctx* ctx, int device,
+                                         const knng_throughput_case* cases, uint64_t num_cases,
+                                         const knng_dataset* queries,
+                                         const knng_search_params* params,
+                                         knng_throughput_row* rows);
+
 /* ---- refine (refine.hpp) ----------------------------------------------- */
 /* partition_dataset refine.cpp:86-126: to_external (n, mem `mem`) and offsets
  * (ranks+1, host).  locals_out (nullable, same mem): all rows in internal

@@ -104,18 +104,47 @@ knng_status guard(F&& f) {
 
 void check_ds(const knng_dataset* ds) {
   require(ds != nullptr && (ds->data != nullptr || ds->n == 0), "knng: null dataset");
-  require(ds->elem_kind == KNNG_ELEM_F32 && ds->metric == KNNG_METRIC_L2,
-          "knng: the B200 path implements f32 / l2 datasets (u8 and cosine are not built yet)");
+  require(ds->elem_kind == KNNG_ELEM_F32 || ds->elem_kind == KNNG_ELEM_U8,
+          "knng: unknown element kind");
+  require(ds->metric == KNNG_METRIC_L2,
+          "knng: the B200 path implements the l2 metric (cosine is not built yet)");
   require(ds->dims >= 1 && ds->dims <= (1u << 20), "knng: dims out of range");
 }
 
-// A dataset resident on the runner's device (copied in if host memory).
+// l2_u8 (core.hpp:32-39) promotes every byte to float before the sequential
+// sum, and (float)a - (float)b and its square are exact: expanding u8 rows to
+// f32 once gives bit-identical distances through the f32 kernels.
+__global__ void k_u8_to_f32(const uint8_t* __restrict__ in, u64 count, float* __restrict__ out) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (u64)gridDim.x * blockDim.x)
+    out[i] = (float)in[i];
+}
+
+// A dataset resident on the runner's device as f32 rows (copied in if host
+// memory, expanded if u8).
 struct DevData {
   DBuf<float> own;
   const float* p = nullptr;
 };
 void stage(Runner& r, const knng_dataset* ds, DevData& out) {
   check_ds(ds);
+  if (ds->elem_kind == KNNG_ELEM_U8) {
+    const u64 cells = ds->n * ds->dims;
+    out.own.alloc(r, cells);
+    out.p = out.own.p;
+    if (!cells) return;
+    DBuf<uint8_t> tmp;
+    const uint8_t* src = static_cast<const uint8_t*>(ds->data);
+    if (ds->mem != KNNG_MEM_DEVICE) {
+      tmp.alloc(r, cells);
+      KNNG_CUDA(cudaMemcpyAsync(tmp.p, ds->data, cells, cudaMemcpyHostToDevice, r.stream));
+      src = tmp.p;
+    }
+    const unsigned g = (unsigned)std::min<u64>(ceil_div<u64>(cells, 256), (u64)r.num_sms * 32);
+    k_u8_to_f32<<<g, 256, 0, r.stream>>>(src, cells, out.own.p);
+    KNNG_LAUNCH_CHECK();
+    return;
+  }
   if (ds->mem == KNNG_MEM_DEVICE) {
     out.p = static_cast<const float*>(ds->data);
     return;
@@ -550,6 +579,70 @@ knng_status knng_ann_search(knng_ctx* ctx, int device, const knng_dataset* queri
   });
 }
 
+knng_status knng_search_throughput_probe(knng_ctx* ctx, int device,
+                                         const knng_throughput_case* cases, uint64_t num_cases,
+                                         const knng_dataset* queries,
+                                         const knng_search_params* params,
+                                         knng_throughput_row* rows) {
+  return guard([&] {
+    Runner& r = ctx->runner(device);
+    DeviceGuard g(r.device);
+    require(queries && params && (cases || num_cases == 0) && (rows || num_cases == 0),
+            "search_throughput_probe: null argument");
+    if (queries->n == 0)
+      throw std::invalid_argument("search_throughput_probe: empty query set");  // :134-135
+    for (uint64_t i = 1; i < num_cases; ++i)
+      if (cases[i].source_count < cases[i - 1].source_count)
+        throw std::invalid_argument("search_throughput_probe: sizes must ascend");  // :136-139
+    const SearchParamsDev sp = to_sp(params);
+    DevData q;
+    stage(r, queries, q);
+    const u64 nq = queries->n, ks = sp.k_s;
+    DBuf<u32> oi(r, nq * ks);
+    DBuf<float> od(r, nq * ks);
+    cudaEvent_t e0, e1;
+    KNNG_CUDA(cudaEventCreate(&e0));
+    KNNG_CUDA(cudaEventCreate(&e1));
+    struct Ev {
+      cudaEvent_t a, b;
+      ~Ev() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
+    } ev{e0, e1};
+    for (uint64_t i = 0; i < num_cases; ++i) {
+      const knng_throughput_case& c = cases[i];
+      require(c.vectors != nullptr && c.sg_ids != nullptr, "search_throughput_probe: null case");
+      require(queries->dims == c.vectors->dims && queries->elem_kind == c.vectors->elem_kind &&
+                  queries->metric == c.vectors->metric,
+              "ann_search: query/vector datasets incompatible");
+      validate_search(queries->dims, c.vectors->dims, c.sg_n, c.vectors->n, sp);
+      DevData v;
+      stage(r, c.vectors, v);
+      DBuf<u32> sgd;
+      const u32* sg = c.sg_ids;
+      if (c.sg_mem != KNNG_MEM_DEVICE) {
+        sgd.alloc(r, c.sg_n * c.degree + 1);
+        copy_in(r, sgd.p, c.sg_ids, c.sg_n * c.degree, false);
+        sg = sgd.p;
+      }
+      r.sync();
+      KNNG_CUDA(cudaEventRecord(e0, r.stream));
+      ann_search_device(r, q.p, nq, (int)queries->dims, sg, (u32)c.degree, v.p, c.vectors->n, sp,
+                        0, oi.p, od.p, nullptr, nullptr, nullptr);
+      KNNG_CUDA(cudaEventRecord(e1, r.stream));
+      KNNG_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      KNNG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      knng_throughput_row& row = rows[i];
+      row.source_count = c.source_count;
+      row.num_queries = nq;
+      row.seconds = ms / 1000.0;
+      row.qps = row.seconds > 0.0 ? (double)nq / row.seconds : 0.0;
+    }
+  });
+}
+
 knng_status knng_partition(knng_ctx* ctx, int device, const knng_dataset* ds, uint64_t ranks,
                            uint64_t seed, uint8_t mem, uint32_t* to_external, uint64_t* offsets,
                            float* locals_out) {
@@ -652,12 +745,21 @@ knng_status knng_build_distributed(knng_ctx* ctx, const knng_dataset* ds,
   return guard([&] {
     require(ctx && ds && cfg && out, "build_distributed: null argument");
     check_ds(ds);
-    const RefineCfg c = to_cfg(cfg);
+    RefineCfg c = to_cfg(cfg);
     require(out->n == ds->n && out->k == c.k, "build_distributed: output shape mismatch");
     DistResult res;
-    build_distributed(ctx->devices, static_cast<const float*>(ds->data), ds->mem == KNNG_MEM_DEVICE,
-                      ds->n, (int)ds->dims, c, out->ids, out->dists, out->mem == KNNG_MEM_DEVICE,
-                      &res);
+    const float* xp = static_cast<const float*>(ds->data);
+    bool x_dev = ds->mem == KNNG_MEM_DEVICE;
+    DevData staged;
+    if (ds->elem_kind == KNNG_ELEM_U8) {  // rows expanded to f32 on device 0
+      stage(ctx->runner(ctx->devices[0]), ds, staged);
+      ctx->runner(ctx->devices[0]).sync();
+      xp = staged.p;
+      x_dev = true;
+      c.u8_elems = true;
+    }
+    build_distributed(ctx->devices, xp, x_dev, ds->n, (int)ds->dims, c, out->ids, out->dists,
+                      out->mem == KNNG_MEM_DEVICE, &res);
     ctx->last_log = res.comm_log;
     fill_dist_result(res, result);
     if (snap_ids && snap_dists) {
@@ -687,10 +789,19 @@ knng_status knng_build_distributed_rank(knng_ctx* ctx, int device, uint64_t rank
     t.user = user;
     t.allgather = allgather;
     DistResult res;
+    const float* xp = static_cast<const float*>(ds->data);
+    bool x_dev = ds->mem == KNNG_MEM_DEVICE;
+    DevData staged;
+    if (ds->elem_kind == KNNG_ELEM_U8) {  // rows expanded to f32 on this rank's device
+      stage(ctx->runner(device), ds, staged);
+      ctx->runner(device).sync();
+      xp = staged.p;
+      x_dev = true;
+      c.u8_elems = true;
+    }
     const uint64_t rows = build_distributed_rank(
-        device, (size_t)rank, (size_t)world_size, t, static_cast<const float*>(ds->data),
-        ds->mem == KNNG_MEM_DEVICE, ds->n, (int)ds->dims, c, out_ids, out_dists, out_rows,
-        out_mem == KNNG_MEM_DEVICE, &res);
+        device, (size_t)rank, (size_t)world_size, t, xp, x_dev, ds->n, (int)ds->dims, c, out_ids,
+        out_dists, out_rows, out_mem == KNNG_MEM_DEVICE, &res);
     if (rows_out) *rows_out = rows;
     ctx->last_log = res.comm_log;
     fill_dist_result(res, result);

@@ -95,7 +95,8 @@ uint64_t effective_groups(const std::vector<uint64_t>& offsets, const RefineCfg&
     for (uint64_t g = 0; g < cfg.groups; ++g)
       span = std::max(span, offsets[(g + 1) * gs] - offsets[g * gs]);
     const uint64_t od = cfg.out_degree ? cfg.out_degree : cfg.k;
-    const uint64_t est = span * ((uint64_t)d * 4 + cfg.k * 8 + od * 4);
+    const uint64_t esz = cfg.u8_elems ? 1 : 4;  // refine.cpp:175-176
+    const uint64_t est = span * ((uint64_t)d * esz + cfg.k * 8 + od * 4);
     if (est > cfg.max_concat_bytes) skip = true;
   }
   return skip ? p : cfg.groups;
@@ -217,7 +218,7 @@ void a2a_refine(Shared& S, RankState& R) {
   optimize_graph_device(r, R.keys.p, R.n_local, (u32)S.k, (u32)S.offsets[R.rank], R.local_x.p,
                         S.d, (u32)S.od, own.p);
   S.world->publish(R.rank, kDataset, R.local_x.p, R.n_local * S.d * 4,
-                   wire_region_size(RegionKind::dataset, R.n_local, S.d), r);
+                   wire_region_size(RegionKind::dataset, R.n_local, S.d, S.cfg->u8_elems), r);
   S.world->publish(R.rank, kSGraph, own.p, R.n_local * S.od * 4,
                    wire_region_size(RegionKind::sgraph, R.n_local, S.od), r);
   S.world->barrier(R.rank, r);
@@ -238,7 +239,7 @@ void a2a_refine(Shared& S, RankState& R) {
 void refine_rank(Shared& S, RankState& R, bool capture) {
   Runner& r = *R.runner;
   S.world->publish(R.rank, kDataset, R.local_x.p, R.n_local * S.d * 4,
-                   wire_region_size(RegionKind::dataset, R.n_local, S.d), r);
+                   wire_region_size(RegionKind::dataset, R.n_local, S.d, S.cfg->u8_elems), r);
   S.world->publish(R.rank, kGraph, R.keys.p, R.n_local * S.k * 8,
                    wire_region_size(RegionKind::knng, R.n_local, S.k), r);
   S.world->barrier(R.rank, r);

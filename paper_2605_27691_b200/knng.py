@@ -159,6 +159,8 @@ _SIGS = {
                                               C.POINTER(_Dataset), C.POINTER(_RefineConfig), _vp,
                                               _vp, _vp, C.c_int, C.POINTER(_u64),
                                               C.POINTER(_DistResult)]),
+    "knng_search_throughput_probe": (C.c_int, [_vp, C.c_int, _vp, _u64, C.POINTER(_Dataset),
+                                               C.POINTER(_SearchParams), _vp]),
     "knng_refine": (C.c_int, [_vp, _vp, _u64, _u64, C.POINTER(_RefineConfig), _vp, _vp, _vp,
                               C.c_int, C.POINTER(_DistResult)]),
     "knng_last_comm_log": (C.c_int, [_vp, _vp, _u64, C.POINTER(_u64)]),
@@ -264,18 +266,29 @@ def _mem(x) -> int:
 
 
 def _as_rows(x):
+    """2-d f32 rows, or u8 rows kept as u8 (ElemKind::u8, core.hpp:14)."""
     if _is_torch_cuda(x):
         import torch
-        assert x.dtype == torch.float32 and x.dim() == 2
+        assert x.dtype in (torch.float32, torch.uint8) and x.dim() == 2
         return x.contiguous()
-    x = np.ascontiguousarray(x, dtype=np.float32)
+    if isinstance(x, np.ndarray) and x.dtype == np.uint8:
+        x = np.ascontiguousarray(x)
+    else:
+        x = np.ascontiguousarray(x, dtype=np.float32)
     if x.ndim != 2:
         raise InvalidArgument("dataset must be a 2-D array (N x dims)")
     return x
 
 
+def _is_u8(x) -> bool:
+    if _is_torch_cuda(x):
+        import torch
+        return x.dtype == torch.uint8
+    return getattr(x, "dtype", None) == np.uint8
+
+
 def _dataset(x, metric: int = 0) -> _Dataset:
-    return _Dataset(_ptr(x), x.shape[0], x.shape[1], 0, metric, _mem(x), 0)
+    return _Dataset(_ptr(x), x.shape[0], x.shape[1], 1 if _is_u8(x) else 0, metric, _mem(x), 0)
 
 
 def _empty_like_mem(x, shape, dtype):
@@ -642,16 +655,64 @@ def ann_search(queries, sgraph, vectors, params: Optional[SearchParams] = None,
     return SearchResult(out_i, out_d, hops, scored)
 
 
+class _ThroughputCase(C.Structure):
+    _fields_ = [("source_count", C.c_uint64), ("sg_ids", C.c_void_p), ("sg_n", C.c_uint64),
+                ("degree", C.c_uint64), ("vectors", C.POINTER(_Dataset)), ("sg_mem", C.c_uint8)]
+
+
+class _ThroughputRow(C.Structure):
+    _fields_ = [("source_count", C.c_uint64), ("num_queries", C.c_uint64),
+                ("seconds", C.c_double), ("qps", C.c_double)]
+
+
+@dataclasses.dataclass
+class ThroughputRow:
+    """annsearch.hpp:59-64"""
+    source_count: int
+    num_queries: int
+    seconds: float
+    qps: float
+
+
+def search_throughput_probe(cases, queries, params: "SearchParams",
+                            device: Optional[int] = None) -> List[ThroughputRow]:
+    """annsearch.cpp:131-155: `cases` = [(source_count, sgraph, vectors), ...]
+    in ascending source_count; seconds are device time of each search."""
+    q = _as_rows(queries)
+    dev = _device_of(q) if device is None else device
+    keep = []
+    arr = (_ThroughputCase * max(1, len(cases)))()
+    for i, (count, sg, vec) in enumerate(cases):
+        v = _as_rows(vec)
+        sgm = sg if _is_torch_cuda(sg) else np.ascontiguousarray(sg, np.uint32)
+        ds = _dataset(v)
+        keep += [v, sgm, ds]
+        arr[i] = _ThroughputCase(count, _ptr(sgm), sgm.shape[0], sgm.shape[1], C.pointer(ds),
+                                 _mem(sgm))
+    rows = (_ThroughputRow * max(1, len(cases)))()
+    qd = _dataset(q)
+    _check(lib().knng_search_throughput_probe(context().h, dev, arr, len(cases), C.byref(qd),
+                                              C.byref(params._c()), rows))
+    return [ThroughputRow(rows[i].source_count, rows[i].num_queries, rows[i].seconds,
+                          rows[i].qps) for i in range(len(cases))]
+
+
 def partition_dataset(x, ranks: int, seed: int, gather: bool = True, device: int = 0) -> Partition:
     """refine.cpp:86-126 (bit-exact permutation computed on the GPU)."""
     x = _as_rows(x)
     n = x.shape[0]
     te = np.empty(max(n, 1), np.uint32)
     off = np.empty(ranks + 1, np.uint64)
-    loc = np.empty_like(x) if (gather and isinstance(x, np.ndarray)) else None
+    host_gather = gather and isinstance(x, np.ndarray)
+    u8 = _is_u8(x)
+    # f32 rows are gathered by the library; u8 rows are gathered here (an
+    # exact byte copy keeps ElemKind::u8, refine.cpp:116-124)
+    loc = np.empty_like(x) if (host_gather and not u8) else None
     ds = _dataset(x)
     _check(lib().knng_partition(context().h, device, C.byref(ds), ranks, seed, MEM_HOST,
                                 _ptr(te), _ptr(off), _ptr(loc)))
+    if host_gather and u8:
+        loc = x[te[:n].astype(np.int64)]
     return Partition(te[:n], off, loc)
 
 

@@ -106,6 +106,25 @@ int main() {
     const KnnGraph g = nn_descent(d, p);
     require(r.graph.ids == g.ids && r.graph.dists == g.dists, "P=1 differs from nn_descent");
   });
+  run("search_throughput_probe (annsearch.cpp:131-155)", [] {
+    const Dataset d = gen_random_dataset(3000, 16, Distribution::clustered, 5, 8);
+    NnDescentParams p;
+    p.k = 16;
+    const KnnGraph g = nn_descent(d, p);
+    const SearchGraph sg = optimize_graph(g, d, 16);
+    const Dataset q = gen_random_dataset(200, 16, Distribution::clustered, 6, 8);
+    SearchParams sp;
+    sp.k_s = 10;
+    const auto rows = search_throughput_probe({{3000, &sg, &d}}, q, sp);
+    require(rows.size() == 1 && rows[0].num_queries == 200 && rows[0].qps > 0, "probe row");
+    bool threw = false;
+    try {
+      search_throughput_probe({{3000, &sg, &d}, {10, &sg, &d}}, q, sp);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    require(threw, "descending sizes must throw");
+  });
   run("one-rank build_distributed_rank == build_distributed P=1 (B200 per-process driver)", [] {
     const Dataset d = gen_random_dataset(2000, 16, Distribution::clustered, 3, 10);
     RefineConfig cfg;
