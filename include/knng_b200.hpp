@@ -509,6 +509,53 @@ inline RankBuildResult build_distributed_rank(const Dataset& d, const RefineConf
   return res;
 }
 
+// read_vecs / write_vecs / read_ivecs / write_ivecs evalio.hpp:17-31
+inline Dataset read_vecs(const std::filesystem::path& path, ElemKind kind,
+                         MetricKind metric = MetricKind::l2) {
+  const int code = kind == ElemKind::f32 ? KNNG_ELEM_F32 : KNNG_ELEM_U8;
+  std::uint64_t rows = 0, dims = 0;
+  detail::check(knng_vecs_shape(path.string().c_str(), code, &rows, &dims));
+  Dataset d = Dataset::empty(dims, kind, metric);
+  d.num_points = rows;
+  void* out;
+  if (kind == ElemKind::f32) {
+    d.f32.resize(rows * dims);
+    out = d.f32.data();
+  } else {
+    d.u8.resize(rows * dims);
+    out = d.u8.data();
+  }
+  detail::check(knng_read_vecs(nullptr, 0, path.string().c_str(), code, out, rows, dims,
+                               KNNG_MEM_HOST));
+  return d;
+}
+inline void write_vecs(const Dataset& d, const std::filesystem::path& path) {
+  const bool f = d.elem_kind == ElemKind::f32;
+  detail::check(knng_write_vecs(path.string().c_str(), f ? KNNG_ELEM_F32 : KNNG_ELEM_U8,
+                                f ? static_cast<const void*>(d.f32.data())
+                                  : static_cast<const void*>(d.u8.data()),
+                                d.num_points, d.dims));
+}
+struct IdMatrix {
+  std::size_t rows = 0;
+  std::size_t cols = 0;
+  std::vector<std::int32_t> v;
+};
+inline IdMatrix read_ivecs(const std::filesystem::path& path) {
+  std::uint64_t rows = 0, cols = 0;
+  detail::check(knng_vecs_shape(path.string().c_str(), KNNG_ELEM_I32, &rows, &cols));
+  IdMatrix m;
+  m.rows = rows;
+  m.cols = cols;
+  m.v.resize(rows * cols);
+  detail::check(knng_read_vecs(nullptr, 0, path.string().c_str(), KNNG_ELEM_I32, m.v.data(), rows,
+                               cols, KNNG_MEM_HOST));
+  return m;
+}
+inline void write_ivecs(const IdMatrix& m, const std::filesystem::path& path) {
+  detail::check(knng_write_vecs(path.string().c_str(), KNNG_ELEM_I32, m.v.data(), m.rows, m.cols));
+}
+
 // evalio.hpp (measurement support)
 enum class Distribution { uniform, gaussian, clustered };
 

@@ -40,6 +40,7 @@ typedef enum {
 
 enum { KNNG_MEM_HOST = 0, KNNG_MEM_DEVICE = 1 };
 enum { KNNG_ELEM_F32 = 0, KNNG_ELEM_U8 = 1 };     /* ElemKind core.hpp:14 */
+enum { KNNG_ELEM_I32 = 2 };                       /* .ivecs payload (IdMatrix, evalio.hpp:26-31) */
 enum { KNNG_METRIC_L2 = 0, KNNG_METRIC_COS = 1 }; /* MetricKind core.hpp:15 */
 
 typedef struct knng_ctx knng_ctx;
@@ -296,6 +297,17 @@ knng_status knng_gen_random_dataset(uint64_t n, uint64_t dims, int dist, uint64_
 knng_status knng_save_graph(const knng_graph* g, const char* path);
 knng_status knng_load_graph_header(const char* path, uint64_t* n, uint64_t* k);
 knng_status knng_load_graph(const char* path, knng_graph* out);
+/* read_vecs / write_vecs / read_ivecs / write_ivecs evalio.cpp:31-123: per row
+ * a little-endian i32 dimension, then the row (.fvecs f32, .bvecs u8, .ivecs
+ * i32 per `elem`).  vecs_shape validates every row (FormatError on a
+ * truncated field/payload, a non-positive or inconsistent dimension) and
+ * returns rows x dims; read_vecs fills rows x dims elements into host memory,
+ * or into device memory through pinned staging buffers (mem = device). */
+knng_status knng_vecs_shape(const char* path, int elem, uint64_t* rows, uint64_t* dims);
+knng_status knng_read_vecs(knng_ctx* ctx, int device, const char* path, int elem, void* out,
+                           uint64_t rows, uint64_t dims, uint8_t mem);
+knng_status knng_write_vecs(const char* path, int elem, const void* data, uint64_t rows,
+                            uint64_t dims);
 
 #ifdef __cplusplus
 }

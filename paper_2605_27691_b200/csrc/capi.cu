@@ -25,6 +25,11 @@ void save_graph(const uint32_t* ids, const float* dists, uint64_t n, uint64_t k,
                 const std::string& path);
 void load_graph_header(const std::string& path, uint64_t* n, uint64_t* k);
 void load_graph(const std::string& path, uint32_t* ids, float* dists, uint64_t n, uint64_t k);
+void vecs_shape(const std::string& path, uint64_t esz, uint64_t* rows, uint64_t* dims);
+void read_vecs(const std::string& path, uint64_t esz, void* out, uint64_t rows, uint64_t dims,
+               const Runner* dev_runner);
+void write_vecs(const std::string& path, const void* data, uint64_t rows, uint64_t dims,
+                uint64_t esz);
 }  // namespace knng_b200
 
 using namespace knng_b200;
@@ -884,6 +889,40 @@ knng_status knng_load_graph(const char* path, knng_graph* out) {
   return guard([&] {
     require(out && out->mem == KNNG_MEM_HOST, "load_graph: host graph expected");
     load_graph(path, out->ids, out->dists, out->n, out->k);
+  });
+}
+
+static uint64_t vecs_esz(int elem) {
+  require(elem == KNNG_ELEM_F32 || elem == KNNG_ELEM_U8 || elem == KNNG_ELEM_I32,
+          "vecs: element kind must be f32 (.fvecs), u8 (.bvecs) or i32 (.ivecs)");
+  return elem == KNNG_ELEM_U8 ? 1 : 4;
+}
+
+knng_status knng_vecs_shape(const char* path, int elem, uint64_t* rows, uint64_t* dims) {
+  return guard([&] {
+    require(path && rows && dims, "vecs: null argument");
+    vecs_shape(path, vecs_esz(elem), rows, dims);
+  });
+}
+
+knng_status knng_read_vecs(knng_ctx* ctx, int device, const char* path, int elem, void* out,
+                           uint64_t rows, uint64_t dims, uint8_t mem) {
+  return guard([&] {
+    require(path && (out || rows == 0), "vecs: null argument");
+    const Runner* r = nullptr;
+    if (mem == KNNG_MEM_DEVICE) {
+      require(ctx != nullptr, "read_vecs: a context is needed for device output");
+      r = &ctx->runner(device);
+    }
+    read_vecs(path, vecs_esz(elem), out, rows, dims, r);
+  });
+}
+
+knng_status knng_write_vecs(const char* path, int elem, const void* data, uint64_t rows,
+                            uint64_t dims) {
+  return guard([&] {
+    require(path && (data || rows == 0), "vecs: null argument");
+    write_vecs(path, data, rows, dims, vecs_esz(elem));
   });
 }
 

@@ -159,6 +159,9 @@ _SIGS = {
                                               C.POINTER(_Dataset), C.POINTER(_RefineConfig), _vp,
                                               _vp, _vp, C.c_int, C.POINTER(_u64),
                                               C.POINTER(_DistResult)]),
+    "knng_vecs_shape": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(_u64), C.POINTER(_u64)]),
+    "knng_read_vecs": (C.c_int, [_vp, C.c_int, C.c_char_p, C.c_int, _vp, _u64, _u64, C.c_uint8]),
+    "knng_write_vecs": (C.c_int, [C.c_char_p, C.c_int, _vp, _u64, _u64]),
     "knng_search_throughput_probe": (C.c_int, [_vp, C.c_int, _vp, _u64, C.POINTER(_Dataset),
                                                C.POINTER(_SearchParams), _vp]),
     "knng_refine": (C.c_int, [_vp, _vp, _u64, _u64, C.POINTER(_RefineConfig), _vp, _vp, _vp,
@@ -653,6 +656,46 @@ def ann_search(queries, sgraph, vectors, params: Optional[SearchParams] = None,
                                  C.byref(p._c()), mem, _ptr(out_i), _ptr(out_d), _ptr(hops),
                                  _ptr(scored)))
     return SearchResult(out_i, out_d, hops, scored)
+
+
+_VECS = {"f32": (0, np.float32), "u8": (1, np.uint8), "i32": (2, np.int32)}
+
+
+def vecs_shape(path, kind: str = "f32"):
+    """(rows, dims) of a .fvecs/.bvecs/.ivecs file, every row validated
+    (evalio.cpp:31-66 checks; FormatError on malformed input)."""
+    code, _ = _VECS[kind]
+    r, d = _u64(0), _u64(0)
+    _check(lib().knng_vecs_shape(os.fsencode(path), code, C.byref(r), C.byref(d)))
+    return r.value, d.value
+
+
+def read_vecs(path, kind: str = "f32", device: Optional[int] = None):
+    """read_vecs / read_ivecs evalio.cpp:31-100 -> numpy (rows x dims), or a
+    CUDA tensor on `device` (streamed through pinned buffers)."""
+    code, dt = _VECS[kind]
+    rows, dims = vecs_shape(path, kind)
+    if device is None:
+        out = np.empty((rows, dims), dt)
+        mem = MEM_HOST
+    else:
+        import torch
+        tdt = {np.float32: torch.float32, np.uint8: torch.uint8, np.int32: torch.int32}[dt]
+        out = torch.empty((rows, dims), dtype=tdt, device=f"cuda:{device}")
+        mem = MEM_DEVICE
+    _check(lib().knng_read_vecs(context().h if device is not None else None,
+                                device or 0, os.fsencode(path), code, _ptr(out), rows, dims, mem))
+    return out
+
+
+def write_vecs(path, x, kind: Optional[str] = None):
+    """write_vecs / write_ivecs evalio.cpp:68-123 (bit-exact round trip)."""
+    x = np.ascontiguousarray(x)
+    kind = kind or {np.dtype(np.float32): "f32", np.dtype(np.uint8): "u8",
+                    np.dtype(np.int32): "i32"}[x.dtype]
+    code, dt = _VECS[kind]
+    x = np.ascontiguousarray(x, dt)
+    _check(lib().knng_write_vecs(os.fsencode(path), code, _ptr(x), x.shape[0], x.shape[1]))
 
 
 class _ThroughputCase(C.Structure):

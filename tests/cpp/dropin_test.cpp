@@ -106,6 +106,34 @@ int main() {
     const KnnGraph g = nn_descent(d, p);
     require(r.graph.ids == g.ids && r.graph.dists == g.dists, "P=1 differs from nn_descent");
   });
+  run("vecs round trip + FormatError (test_evalio.cpp semantics, evalio.cpp:31-123)", [] {
+    const auto dir = std::filesystem::temp_directory_path();
+    const Dataset d = gen_random_dataset(50, 7, Distribution::gaussian, 9);
+    write_vecs(d, dir / "knng_dropin.fvecs");
+    const Dataset e = read_vecs(dir / "knng_dropin.fvecs", ElemKind::f32);
+    require(e.num_points == 50 && e.dims == 7 && e.f32 == d.f32, "fvecs round trip");
+    IdMatrix m;
+    m.rows = 3;
+    m.cols = 2;
+    m.v = {1, 2, 3, 4, 5, 6};
+    write_ivecs(m, dir / "knng_dropin.ivecs");
+    require(read_ivecs(dir / "knng_dropin.ivecs").v == m.v, "ivecs round trip");
+    {
+      std::FILE* f = std::fopen((dir / "knng_dropin_bad.fvecs").string().c_str(), "wb");
+      const int dim = 4;
+      const float row[2] = {1.f, 2.f};
+      std::fwrite(&dim, 4, 1, f);
+      std::fwrite(row, 4, 2, f);  // payload shorter than the dimension
+      std::fclose(f);
+    }
+    bool threw = false;
+    try {
+      read_vecs(dir / "knng_dropin_bad.fvecs", ElemKind::f32);
+    } catch (const FormatError&) {
+      threw = true;
+    }
+    require(threw, "truncated payload must throw FormatError");
+  });
   run("search_throughput_probe (annsearch.cpp:131-155)", [] {
     const Dataset d = gen_random_dataset(3000, 16, Distribution::clustered, 5, 8);
     NnDescentParams p;

@@ -22,3 +22,16 @@ def test_search_throughput_probe(knng):
         knng.search_throughput_probe(cases[::-1], q, sp)
     with pytest.raises(knng.InvalidArgument):
         knng.search_throughput_probe(cases, np.zeros((0, 16), np.float32), sp)
+
+
+def test_read_vecs_to_device(knng, tmp_path):
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=(400001, 24)).astype(np.float32)  # 38 MB: more than one staging buffer
+    p = str(tmp_path / "x.fvecs")
+    knng.write_vecs(p, x)
+    y = knng.read_vecs(p, "f32", device=0)
+    assert y.is_cuda and np.array_equal(y.cpu().numpy().view(np.uint32), x.view(np.uint32))
+    b = rng.integers(0, 256, size=(5000, 96)).astype(np.uint8)
+    knng.write_vecs(str(tmp_path / "b.bvecs"), b)
+    z = knng.read_vecs(str(tmp_path / "b.bvecs"), "u8", device=0)
+    assert np.array_equal(z.cpu().numpy(), b)
