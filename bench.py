@@ -554,7 +554,7 @@ def run_multi(args, ws, rank, dist):
         out = step(x_np_pinned)
         e2e.append(time.perf_counter() - t)
     e2e_ms, = allreduce(dist, [1000.0 * statistics.mean(e2e)])
-    h2d = ws * n * DIMS * 4        # every rank receives the dataset
+    h2d = n * DIMS * 4             # each rank reads its block from pinned memory (zero-copy)
     d2h = n * K * 8 + n * 4        # all ranks' rows: ids + dists + external row ids
     del out
 

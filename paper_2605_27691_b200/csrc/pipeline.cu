@@ -583,9 +583,19 @@ uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const Hos
   DBuf<float> xdev;
   const float* Xd = X;
   if (!x_on_device) {
-    xdev.alloc(r, n * d);
-    KNNG_CUDA(cudaMemcpyAsync(xdev.p, X, n * (uint64_t)d * 4, cudaMemcpyHostToDevice, r.stream));
-    Xd = xdev.p;
+    // A rank needs only its own block (remote rows arrive over NVLink from
+    // their owners): from pinned host memory it gathers those rows directly
+    // (zero-copy over PCIe, 1/P of the dataset); pageable memory is copied.
+    void* mapped = nullptr;
+    if (cudaHostGetDevicePointer(&mapped, const_cast<float*>(X), 0) == cudaSuccess && mapped) {
+      Xd = static_cast<const float*>(mapped);
+    } else {
+      cudaGetLastError();
+      xdev.alloc(r, n * d);
+      KNNG_CUDA(cudaMemcpyAsync(xdev.p, X, n * (uint64_t)d * 4, cudaMemcpyHostToDevice,
+                                r.stream));
+      Xd = xdev.p;
+    }
   }
   // every rank computes the same permutation (refine.cpp:86-126, bit-exact)
   DBuf<u32> to_ext(r, n);

@@ -33,6 +33,13 @@ def _rank_main(rank, world, port, n, d, out_dir):
                             search=knng.SearchParams(k_s=16, beam_width=64, num_entry_points=32,
                                                      seed=5))
     r = knng.build_distributed_rank(x, cfg, rank, world)
+    # the same rank from pinned host memory (each rank gathers only its block
+    # over PCIe) must give the identical rows
+    xh = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+    xh.copy_(x.cpu())
+    rh = knng.build_distributed_rank(xh.numpy(), cfg, rank, world, device=dev)
+    assert np.array_equal(rh.graph.ids, r.graph.ids.cpu().numpy())
+    assert np.array_equal(rh.rows, r.rows.cpu().numpy())
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=r.graph.ids.cpu().numpy(),
              dists=r.graph.dists.cpu().numpy(), rows=r.rows.cpu().numpy(),
              gets=np.array([[g.src, g.target, g.bytes, g.epoch] for g in r.comm_log], np.uint64))
