@@ -30,6 +30,7 @@ cpu_baseline: the reference's own CPU nn_descent (oracle/_ref, compiled from
          workload, all host threads (rank 0, N = 1 only).
 """
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -70,6 +71,8 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        if os.environ.get("KNNG_BENCH_NO_SMI"):
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
@@ -250,6 +253,11 @@ def main():
     ap.add_argument("--no-ramp", action="store_true", help="skip the clock ramp (profiling runs)")
     ap.add_argument("--per-gpu", type=int, default=PER_GPU)
     args = ap.parse_args()
+    # a full collection of the interpreter's (torch-sized) heap between two
+    # builds leaves the GPU idle inside the timed region: collect now, then
+    # keep the collector off for the run
+    gc.collect()
+    gc.disable()
     ws, rank = dist_env()
     if args.impl == "reference":
         return run_reference_arm(args, ws, rank)
@@ -395,7 +403,7 @@ def main():
         # dim, no FMA -- parity forbids reassociation/contraction), not HBM:
         # report that roofline too (non-FMA fp32 peak = SMs x 128 x clock)
         join_ops = st.pairs * DIMS * 3
-        fp32_peak = 148 * 128 * clocks.summary().get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        fp32_peak = 148 * 128 * (clocks.summary().get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
         line["roofline"] = {"kernel": "k_join (nndescent.cu)", "bound": "hbm",
                             "achieved": achieved, "peak": peak, "unit": "GB/s",
                             "frac": achieved / peak, "traffic": traffic,

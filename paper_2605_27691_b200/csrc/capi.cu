@@ -164,9 +164,11 @@ void stage(Runner& r, const knng_dataset* ds, DevData& out) {
 template <class T>
 void copy_out(Runner& r, T* dst, const T* src, size_t count, bool dst_on_device) {
   if (!count) return;
-  KNNG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T),
-                            dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                            r.stream));
+  if (!dst_on_device) {
+    d2h_host(r, dst, src, count * sizeof(T));
+    return;
+  }
+  KNNG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToDevice, r.stream));
 }
 template <class T>
 void copy_in(Runner& r, T* dst, const T* src, size_t count, bool src_on_device) {

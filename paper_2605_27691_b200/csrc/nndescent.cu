@@ -566,8 +566,23 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   // Offer queue: each point chunk owns a region sized for its worst case (2
   // offers per pair, max pairs C(2B,2) + 2B(k+B)), so nothing can overflow;
   // points are processed in slices to bound the queue (budget below).
+  // memory available to stream-ordered allocations: free device memory plus
+  // what the pool holds unused from earlier calls (cudaMemGetInfo counts that
+  // as used, so the budget -- and the queue size -- drifted between builds
+  // and a later build had to map tens of GB afresh)
   size_t free_b = 0, total_b = 0;
   KNNG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  {
+    cudaMemPool_t pool;
+    uint64_t reserved = 0, used = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, r.device) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) ==
+            cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+        reserved > used)
+      free_b += reserved - used;
+    cudaGetLastError();
+  }
   // up to 64 GB of worst-case queue (B200: 180 GB HBM): C2 runs as a single
   // slice (one join + one offer launch per iteration)
   const u64 budget = std::min<u64>(64ull << 30, free_b / 3);

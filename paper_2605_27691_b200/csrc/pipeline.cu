@@ -363,8 +363,8 @@ void translate_all(Runner& r0, std::vector<RankState>& ranks, const std::vector<
     DBuf<u32> ti(r0, n * k);
     DBuf<float> td(r0, n * k);
     translate_device(r0, all.p, n, (u32)k, to_ext, ti.p, td.p);
-    KNNG_CUDA(cudaMemcpyAsync(out_ids, ti.p, n * k * 4, cudaMemcpyDeviceToHost, r0.stream));
-    KNNG_CUDA(cudaMemcpyAsync(out_d, td.p, n * k * 4, cudaMemcpyDeviceToHost, r0.stream));
+    d2h_host(r0, out_ids, ti.p, n * k * 4);
+    d2h_host(r0, out_d, td.p, n * k * 4);
   }
   r0.sync();
 }
@@ -626,11 +626,9 @@ uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const Hos
     DBuf<float> td(r, R.n_local * S.k);
     translate_rows_device(r, R.keys.p, R.n_local, (u32)S.k, to_ext.p, offsets[rank], ti.p, td.p,
                           tr.p);
-    KNNG_CUDA(cudaMemcpyAsync(out_ids, ti.p, R.n_local * S.k * 4, cudaMemcpyDeviceToHost,
-                              r.stream));
-    KNNG_CUDA(cudaMemcpyAsync(out_dists, td.p, R.n_local * S.k * 4, cudaMemcpyDeviceToHost,
-                              r.stream));
-    KNNG_CUDA(cudaMemcpyAsync(out_rows, tr.p, R.n_local * 4, cudaMemcpyDeviceToHost, r.stream));
+    d2h_host(r, out_ids, ti.p, R.n_local * S.k * 4);
+    d2h_host(r, out_dists, td.p, R.n_local * S.k * 4);
+    d2h_host(r, out_rows, tr.p, R.n_local * 4);
   }
   r.sync();
   if (res) {

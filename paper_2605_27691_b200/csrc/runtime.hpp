@@ -265,6 +265,49 @@ struct HBuf {
   }
 };
 
+// Device -> pageable host, synchronous: 16 MB chunks through two pinned pool
+// buffers, the copy of chunk i overlapping the host memcpy of chunk i - 1
+// (a direct copy into pageable memory measured ~4 GB/s).  Pinned
+// destinations take the direct path.
+inline void d2h_host(const Runner& r, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  cudaPointerAttributes at{};
+  const bool pinned =
+      cudaPointerGetAttributes(&at, dst) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  constexpr size_t kChunk = size_t{16} << 20;
+  if (pinned || bytes <= kChunk) {
+    KNNG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, r.stream));
+    r.sync();
+    return;
+  }
+  HBuf<char> buf[2];
+  buf[0].alloc(kChunk);
+  buf[1].alloc(kChunk);
+  cudaEvent_t ev[2];
+  KNNG_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  KNNG_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  const char* s = static_cast<const char*>(src);
+  char* d = static_cast<char*>(dst);
+  size_t prev_off = 0, prev_len = 0;
+  int i = 0;
+  for (size_t off = 0; off < bytes; off += kChunk, ++i) {
+    const size_t len = std::min(kChunk, bytes - off);
+    KNNG_CUDA(cudaMemcpyAsync(buf[i & 1].p, s + off, len, cudaMemcpyDeviceToHost, r.stream));
+    KNNG_CUDA(cudaEventRecord(ev[i & 1], r.stream));
+    if (i > 0) {
+      KNNG_CUDA(cudaEventSynchronize(ev[(i - 1) & 1]));
+      std::memcpy(d + prev_off, buf[(i - 1) & 1].p, prev_len);
+    }
+    prev_off = off;
+    prev_len = len;
+  }
+  KNNG_CUDA(cudaEventSynchronize(ev[(i - 1) & 1]));
+  std::memcpy(d + prev_off, buf[(i - 1) & 1].p, prev_len);
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+}
+
 // Grid of persistent CTAs: `per_sm` resident CTAs on every SM.
 inline unsigned persistent_grid(const Runner& r, int per_sm, uint64_t work_items) {
   uint64_t g = (uint64_t)r.num_sms * (uint64_t)per_sm;
