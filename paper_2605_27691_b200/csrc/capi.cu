@@ -37,10 +37,22 @@ using namespace knng_b200;
 struct knng_ctx {
   std::vector<int> devices;
   std::vector<std::unique_ptr<Runner>> runners;  // one default runner per device
+  // per-device NN-descent workspaces (declared after the runners: destroyed
+  // first, while their streams exist)
+  std::vector<std::unique_ptr<NndWorkspace>> nnd_ws;
   std::vector<GetRecord> last_log;
   Runner& runner(int dev) {
     for (size_t i = 0; i < devices.size(); ++i)
       if (devices[i] == dev) return *runners[i];
+    throw std::invalid_argument("knng: device " + std::to_string(dev) + " not in this context");
+  }
+  NndWorkspace* workspace(int dev) {
+    for (size_t i = 0; i < devices.size(); ++i)
+      if (devices[i] == dev) {
+        if (nnd_ws.size() < devices.size()) nnd_ws.resize(devices.size());
+        if (!nnd_ws[i]) nnd_ws[i] = std::make_unique<NndWorkspace>();
+        return nnd_ws[i].get();
+      }
     throw std::invalid_argument("knng: device " + std::to_string(dev) + " not in this context");
   }
 };
@@ -462,7 +474,8 @@ knng_status knng_nn_descent(knng_ctx* ctx, int device, const knng_dataset* ds,
     DBuf<u32> flags(r, n);
     NndStats st;
     tr.mark("alloc");
-    nn_descent_device(r, DevRows{x.p, n, (int)ds->dims}, p, keys.p, flags.p, &st, stats != nullptr);
+    nn_descent_device(r, DevRows{x.p, n, (int)ds->dims}, p, keys.p, flags.p, &st, stats != nullptr,
+                      ctx->workspace(device));
     tr.mark("build");
     const bool dev = out->mem == KNNG_MEM_DEVICE;
     if (dev) {
@@ -808,7 +821,8 @@ knng_status knng_build_distributed_rank(knng_ctx* ctx, int device, uint64_t rank
     }
     const uint64_t rows = build_distributed_rank(
         device, (size_t)rank, (size_t)world_size, t, xp, x_dev, ds->n, (int)ds->dims, c, out_ids,
-        out_dists, out_rows, out_mem == KNNG_MEM_DEVICE, &res);
+        out_dists, out_rows, out_mem == KNNG_MEM_DEVICE, &res, &ctx->runner(device),
+        ctx->workspace(device));
     if (rows_out) *rows_out = rows;
     ctx->last_log = res.comm_log;
     fill_dist_result(res, result);

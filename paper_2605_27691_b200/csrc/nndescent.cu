@@ -449,11 +449,21 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
                  const uint64_t* keys, uint32_t* flags, SampleLists& s, RevCsr& c, bool prune_old,
                  uint64_t* launches) {
   const unsigned g = warp_grid(r, n);
+  double t_lap = slow_trace_on() ? trace_clock_ms() : 0;
+  auto lap = [&](const char* what) {
+    if (!slow_trace_on()) return;
+    const double t = trace_clock_ms();
+    if (t - t_lap > 5.0)
+      std::fprintf(stderr, "[knng slow] t %.1f dev %d sample_into %s host %.1f ms\n", t, r.device,
+                   what, t - t_lap);
+    t_lap = t;
+  };
   c.cnt_new.zero();
   c.cnt_old.zero();
   k_sample_fwd<<<g, 256, 0, r.stream>>>(keys, flags, n, k, B, iter_seed, s.nf.p, s.nfn.p,
                                         s.of.p, s.ofn.p, c.cnt_new.p, c.cnt_old.p, !prune_old);
   KNNG_LAUNCH_CHECK();
+  lap("zero+sample_fwd");
   if (prune_old) {
     k_old_count<<<g, 256, 0, r.stream>>>(n, k, s.of.p, s.ofn.p, s.nfn.p, c.cnt_new.p,
                                          c.src_cnt.p, c.cnt_old.p);
@@ -462,9 +472,11 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
   } else {
     exclusive_scan_u32(r, s.ofn.p, c.src_off_old.p, n);
   }
+  lap("old_count+scan");
   exclusive_scan_u32(r, s.nfn.p, c.src_off_new.p, n);
   exclusive_scan_u32(r, c.cnt_new.p, c.off_new.p, n);
   exclusive_scan_u32(r, c.cnt_old.p, c.off_old.p, n);
+  lap("scans");
   k_emit_pairs<<<g, 256, 0, r.stream>>>(n, B, s.nf.p, s.nfn.p, c.src_off_new.p, nullptr, nullptr,
                                         c.key_new.p, c.val_new.p);
   KNNG_LAUNCH_CHECK();
@@ -473,6 +485,7 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
                                         prune_old ? c.cnt_new.p : nullptr, c.key_old.p,
                                         c.val_old.p);
   KNNG_LAUNCH_CHECK();
+  lap("emit");
   // sorts read their element counts (src_off[n]) on the device: no host sync
   bool tn = false, to = false;
   const u32 maxk = (u32)(n ? n - 1 : 0);
@@ -480,6 +493,7 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
                        c.src_off_new.p + n, maxk, &tn);
   radix_sort_pairs_dev(r, c.key_old.p, c.val_old.p, c.tk_old.p, c.tv_old.p, n * k,
                        c.src_off_old.p + n, maxk, &to);
+  lap("sorts");
   k_rev_select<<<g, 256, 0, r.stream>>>(n, B, iter_seed, c.off_new.p, tn ? c.tv_new.p : c.val_new.p,
                                         c.off_old.p, to ? c.tv_old.p : c.val_old.p, s.nr.p,
                                         s.nrn.p, s.orv.p, s.orn.p);
@@ -529,8 +543,18 @@ void sample_neighbors_device(Runner& r, uint64_t n, uint32_t k, double rho, uint
               nullptr);
 }
 
+namespace {
+// buffer of at least `count` entries: the workspace's (grown if short) or `own`
+template <class T>
+T* ws_buf(Runner& r, DBuf<T>* ws, DBuf<T>& own, uint64_t count) {
+  DBuf<T>& b = ws ? *ws : own;
+  if (b.n < count) b.alloc(r, count);
+  return b.p;
+}
+}  // namespace
+
 void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_t* keys,
-                       uint32_t* flags, NndStats* st, bool time_kernels) {
+                       uint32_t* flags, NndStats* st, bool time_kernels, NndWorkspace* ws) {
   validate_nnd(p, ds.n);
   const u64 n = ds.n;
   const u32 k = p.k;
@@ -545,8 +569,9 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   const auto t_call = std::chrono::steady_clock::now();
 
   DBuf<float> worst(r, n);
-  DBuf<u64> slots(r, n * S);
-  slots.fill_bytes(0xff);
+  DBuf<u64> slots_own;
+  u64* slots_p = ws_buf(r, ws ? &ws->slots : nullptr, slots_own, n * S);
+  KNNG_CUDA(cudaMemsetAsync(slots_p, 0xff, n * S * sizeof(u64), r.stream));
   DBuf<u64> counters(r, kNumCounters);
   HBuf<u64> hcount(kNumCounters);
   SampleLists s;
@@ -562,7 +587,8 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
 
   // join lists (compact per point) + join launch shape
   const JoinPlan plan = plan_join(r, ds.d, k, B);
-  DBuf<u32> L_ids(r, n * plan.RMAX), L_cnt(r, n);
+  DBuf<u32> L_ids_own, L_cnt(r, n);
+  u32* L_ids_p = ws_buf(r, ws ? &ws->L_ids : nullptr, L_ids_own, n * plan.RMAX);
   // Offer queue: each point chunk owns a region sized for its worst case (2
   // offers per pair, max pairs C(2B,2) + 2B(k+B)), so nothing can overflow;
   // points are processed in slices to bound the queue (budget below).
@@ -583,6 +609,7 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
       free_b += reserved - used;
     cudaGetLastError();
   }
+  if (ws) free_b += ws->q_key.n * 8 + ws->q_tgt.n * 4;  // reused below
   // up to 64 GB of worst-case queue (B200: 180 GB HBM): C2 runs as a single
   // slice (one join + one offer launch per iteration)
   const u64 budget = std::min<u64>(64ull << 30, free_b / 3);
@@ -592,8 +619,10 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
     slice = n;
     chunks_per_slice = ceil_div<u64>(n, (u64)kJoinChunk);
   }
-  DBuf<u64> q_key(r, chunks_per_slice * plan.q_per_chunk);
-  DBuf<u32> q_tgt(r, chunks_per_slice * plan.q_per_chunk), q_fill(r, chunks_per_slice);
+  DBuf<u64> q_key_own;
+  DBuf<u32> q_tgt_own, q_fill(r, chunks_per_slice);
+  u64* q_key_p = ws_buf(r, ws ? &ws->q_key : nullptr, q_key_own, chunks_per_slice * plan.q_per_chunk);
+  u32* q_tgt_p = ws_buf(r, ws ? &ws->q_tgt : nullptr, q_tgt_own, chunks_per_slice * plan.q_per_chunk);
   DBuf<u32> chunk_ctr(r, 1);
   // points with a new entry, compacted: late iterations join a small fraction
   DBuf<u32> act(r, n), act_flag(r, n);
@@ -602,12 +631,12 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   jl.act = act.p;
   jl.X = ds.x;
   jl.d = ds.d;
-  jl.L_ids = L_ids.p;
+  jl.L_ids = L_ids_p;
   jl.L_cnt = L_cnt.p;
   jl.worst = worst.p;
   jl.chunk_counter = chunk_ctr.p;
-  jl.q_key = q_key.p;
-  jl.q_tgt = q_tgt.p;
+  jl.q_key = q_key_p;
+  jl.q_tgt = q_tgt_p;
   jl.q_fill = q_fill.p;
   jl.counters = counters.p;
 
@@ -619,7 +648,7 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
     sample_into(r, n, k, B, iter_seed, keys, flags, s, c, true, &launches);
     tm.tick(kStSample);
     launch_join_lists(r, n, k, B, plan.RMAX, s.nf.p, s.nfn.p, s.of.p, s.ofn.p, s.nr.p, s.nrn.p,
-                      s.orv.p, s.orn.p, L_ids.p, L_cnt.p);
+                      s.orv.p, s.orn.p, L_ids_p, L_cnt.p);
     ++launches;
     tm.tick(kStLists);
     build_active_list(r, n, L_cnt.p, act_flag.p, act_off.p, act.p);
@@ -636,13 +665,13 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
       tm.tick(kStLists);
       launch_join(r, plan, jl);
       tm.tick(kStJoin);
-      launch_offer(r, plan, q_key.p, q_tgt.p, q_fill.p,
-                   (u32)ceil_div<u64>(jl.p_hi - jl.p_lo, (u64)kJoinChunk), slots.p, S, nb, ways,
+      launch_offer(r, plan, q_key_p, q_tgt_p, q_fill.p,
+                   (u32)ceil_div<u64>(jl.p_hi - jl.p_lo, (u64)kJoinChunk), slots_p, S, nb, ways,
                    counters.p, jl.p_lo, jl.n_live);
       tm.tick(kStOffer);
       launches += 2;
     }
-    k_apply<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst.p, slots.p,
+    k_apply<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst.p, slots_p,
                                                    counters.p);
     KNNG_LAUNCH_CHECK();
     launches += 1;

@@ -68,9 +68,18 @@ struct DevRows {
 
 void validate_nnd(const NndParams& p, uint64_t n);
 
+// Grow-only buffers of a build (offer queue, candidate buckets, join lists),
+// kept by a context across builds on one device: a fresh ~50 GB set per build
+// occasionally made the pool map memory anew while the GPU waited.
+struct NndWorkspace {
+  DBuf<uint64_t> q_key, slots;
+  DBuf<uint32_t> q_tgt, L_ids;
+};
+
 // Full build.  keys/flags must hold n*k / n entries on the runner's device.
 void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_t* keys,
-                       uint32_t* flags, NndStats* stats, bool time_kernels);
+                       uint32_t* flags, NndStats* stats, bool time_kernels,
+                       NndWorkspace* ws = nullptr);
 
 // Individual stages (exposed for parity tests through the C-ABI).
 void init_random_graph_device(Runner& r, const DevRows& ds, uint32_t k, uint64_t seed,

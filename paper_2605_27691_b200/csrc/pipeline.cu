@@ -64,6 +64,7 @@ struct RankState {
   double local_t = 0, tree_t = 0, merge_t = 0, flat_t = 0;
   NndStats nst;
   SearchCounters sc;
+  NndWorkspace* ws = nullptr;  // reusable local-build buffers (per-rank driver)
 };
 
 uint64_t size_of(const Shared& S, uint64_t r) { return S.offsets[r + 1] - S.offsets[r]; }
@@ -284,7 +285,7 @@ void local_build_rank(Shared& S, const RefineCfg& cfg, RankState& R) {
   np.seed = p == 1 ? cfg.nn.seed : mix_seed(cfg.nn.seed, R.rank);  // refine.cpp:385
   DBuf<u32> flags(r, R.n_local);
   nn_descent_device(r, DevRows{R.local_x.p, R.n_local, S.d}, np, R.keys.p, flags.p, &R.nst,
-                    true);
+                    true, R.ws);
   shift_ids_device(r, R.keys.p, R.n_local * S.k, (int64_t)S.offsets[R.rank]);
   r.sync();
   R.local_t = now_s() - t;
@@ -564,7 +565,8 @@ void refine_from_local(const std::vector<int>& devices, const float* X_perm, uin
 uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const HostTransport& t,
                                 const float* X, bool x_on_device, uint64_t n, int d,
                                 const RefineCfg& cfg_in, uint32_t* out_ids, float* out_dists,
-                                uint32_t* out_rows, bool out_on_device, DistResult* res) {
+                                uint32_t* out_rows, bool out_on_device, DistResult* res,
+                                Runner* base, NndWorkspace* ws) {
   RefineCfg cfg = cfg_in;
   cfg.ranks = ranks;
   require(rank < ranks, "build_distributed: rank out of range");
@@ -575,7 +577,11 @@ uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const Hos
   std::vector<RankState> one(1);
   RankState& R = one[0];
   R.rank = rank;
-  R.runner = std::make_unique<Runner>(device);
+  // on the caller's persistent stream when given (its workspace buffers are
+  // stream-ordered on it), else a fresh one
+  R.runner = base ? std::make_unique<Runner>(base->device, base->stream)
+                  : std::make_unique<Runner>(device);
+  R.ws = ws;
   Runner& r = *R.runner;
   DeviceGuard g(r.device);
   const double t0 = now_s();

@@ -69,7 +69,8 @@ void build_distributed(const std::vector<int>& devices, const float* X, bool x_o
 uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const HostTransport& t,
                                 const float* X, bool x_on_device, uint64_t n, int d,
                                 const RefineCfg& cfg, uint32_t* out_ids, float* out_dists,
-                                uint32_t* out_rows, bool out_on_device, DistResult* res);
+                                uint32_t* out_rows, bool out_on_device, DistResult* res,
+                                Runner* base = nullptr, NndWorkspace* ws = nullptr);
 
 // Refinement only, from given local graphs (internal global ids, rank blocks
 // at offsets) -- the world-level drivers binary_tree_refine -> grouped_merge

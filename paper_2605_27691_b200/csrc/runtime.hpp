@@ -88,6 +88,11 @@ struct Runner {
     uint64_t thr = ~0ull;
     KNNG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   }
+  // non-owning view of an existing stream (own scratch, the stream stays
+  // with its owner)
+  Runner(int dev, cudaStream_t s) : device(dev), stream(s), owns(false) {
+    KNNG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
   Runner(const Runner&) = delete;
   Runner& operator=(const Runner&) = delete;
   Runner(Runner&& o) noexcept { *this = std::move(o); }
