@@ -642,6 +642,12 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
 
   if (st) *st = NndStats{};
   const double threshold = p.delta * (double)k * (double)n;
+  cudaEvent_t iter_done;
+  KNNG_CUDA(cudaEventCreateWithFlags(&iter_done, cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t e;
+    ~EvGuard() { cudaEventDestroy(e); }
+  } iter_done_guard{iter_done};
   for (u64 iter = 0; iter < p.max_iters; ++iter) {
     counters.zero();
     const u64 iter_seed = mix_seed(p.seed, 0x5a3f1e00ull + iter);
@@ -678,7 +684,13 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
     tm.tick(kStApply);
     KNNG_CUDA(cudaMemcpyAsync(hcount.p, counters.p, kNumCounters * sizeof(u64),
                               cudaMemcpyDeviceToHost, r.stream));
-    r.sync();
+    // busy-poll the iteration's end: a sleeping cudaStreamSynchronize woke
+    // up late now and then, idling the GPU before the next iteration (up to
+    // ~7 ms per iteration, seen as a variable 'sample' stage)
+    KNNG_CUDA(cudaEventRecord(iter_done, r.stream));
+    while (cudaEventQuery(iter_done) == cudaErrorNotReady) {
+    }
+    KNNG_CUDA(cudaGetLastError());
     tm.tick(kStSync);
     const u64 accepted = hcount.p[kCntAccepted];
     if (std::getenv("KNNG_TRACE"))
