@@ -45,6 +45,12 @@ const char* kDataset = "dataset";
 const char* kGraph = "graph";
 const char* kSGraph = "sgraph";
 
+// a rank's runner: owned (fresh stream) or borrowed (the caller's persistent
+// one, whose scratch buffers then survive across builds)
+using RunnerPtr = std::unique_ptr<Runner, void (*)(Runner*)>;
+RunnerPtr owned_runner(int dev) { return RunnerPtr(new Runner(dev), [](Runner* p) { delete p; }); }
+RunnerPtr borrowed_runner(Runner* r) { return RunnerPtr(r, [](Runner*) {}); }
+
 struct Shared {
   const RefineCfg* cfg = nullptr;
   std::vector<uint64_t> offsets;
@@ -56,7 +62,7 @@ struct Shared {
 
 struct RankState {
   size_t rank = 0;
-  std::unique_ptr<Runner> runner;
+  RunnerPtr runner{nullptr, [](Runner*) {}};
   DBuf<float> local_x;
   uint64_t n_local = 0;
   DBuf<u64> keys;  // graph rows in internal global ids
@@ -443,7 +449,7 @@ void build_distributed(const std::vector<int>& devices, const float* X, bool x_o
   for (uint64_t i = 0; i < p; ++i) {
     RankState& R = ranks[i];
     R.rank = i;
-    R.runner = std::make_unique<Runner>(devices[i % devices.size()]);
+    R.runner = owned_runner(devices[i % devices.size()]);
     R.n_local = size_of(S, i);
     R.local_x.alloc(*R.runner, R.n_local * d);
     R.keys.alloc(*R.runner, R.n_local * S.k);
@@ -518,7 +524,7 @@ void refine_from_local(const std::vector<int>& devices, const float* X_perm, uin
   for (uint64_t i = 0; i < p; ++i) {
     RankState& R = ranks[i];
     R.rank = i;
-    R.runner = std::make_unique<Runner>(devices[i % devices.size()]);
+    R.runner = owned_runner(devices[i % devices.size()]);
     Runner& r = *R.runner;
     DeviceGuard g(r.device);
     R.n_local = size_of(S, i);
@@ -577,10 +583,9 @@ uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const Hos
   std::vector<RankState> one(1);
   RankState& R = one[0];
   R.rank = rank;
-  // on the caller's persistent stream when given (its workspace buffers are
-  // stream-ordered on it), else a fresh one
-  R.runner = base ? std::make_unique<Runner>(base->device, base->stream)
-                  : std::make_unique<Runner>(device);
+  // on the caller's persistent runner when given (its workspace and scratch
+  // buffers are stream-ordered on it and reused across builds), else a fresh one
+  R.runner = base ? borrowed_runner(base) : owned_runner(device);
   R.ws = ws;
   Runner& r = *R.runner;
   DeviceGuard g(r.device);

@@ -45,7 +45,12 @@ struct RegionCache {
       }
     }
     void* p = nullptr;
+    const double t0 = trace_clock_ms();
     KNNG_CUDA(cudaMalloc(&p, bytes));
+    if (slow_trace_on())
+      std::fprintf(stderr, "[knng slow] t %.1f region cudaMalloc %llu MB on dev %d: %.1f ms\n",
+                   trace_clock_ms(), (unsigned long long)(bytes >> 20), dev,
+                   trace_clock_ms() - t0);
     *got = bytes;
     return p;
   }
@@ -70,7 +75,11 @@ struct RegionCache {
     }
     for (const Entry& e : evict) {
       DeviceGuard g(e.dev);
+      const double t0 = trace_clock_ms();
       cudaFree(e.p);
+      if (slow_trace_on())
+        std::fprintf(stderr, "[knng slow] t %.1f region cudaFree %llu MB: %.1f ms\n",
+                     trace_clock_ms(), (unsigned long long)(e.bytes >> 20), trace_clock_ms() - t0);
     }
   }
 };
@@ -96,7 +105,11 @@ struct IpcMaps {
     std::memcpy(&h, handle, sizeof(h));
     void* p = nullptr;
     DeviceGuard g(dev);
+    const double t0 = trace_clock_ms();
     KNNG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    if (slow_trace_on())
+      std::fprintf(stderr, "[knng slow] t %.1f ipc open on dev %d: %.1f ms (%zu maps)\n",
+                   trace_clock_ms(), dev, trace_clock_ms() - t0, open.size() + 1);
     open[key] = p;
     return p;
   }
