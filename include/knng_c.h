@@ -158,6 +158,9 @@ const char* knng_last_error(void);
 uint64_t knng_kernel_launches(void);
 /* num_devices <= 0: every visible device.  Enables NVLink peer access. */
 knng_status knng_ctx_create(int num_devices, knng_ctx** out);
+/* A context on the listed devices only (e.g. one process per GPU: its own
+ * device; peers are reached through IPC mappings, not contexts). */
+knng_status knng_ctx_create_on(const int* devices, int num_devices, knng_ctx** out);
 void knng_ctx_destroy(knng_ctx* ctx);
 knng_status knng_ctx_device_count(knng_ctx* ctx, int* out);
 /* The stream calls on `device` run on (for CUDA-event timing by callers). */

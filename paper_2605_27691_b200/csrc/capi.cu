@@ -280,22 +280,25 @@ uint64_t knng_kernel_launches(void) { return launch_counter().load(std::memory_o
 
 const char* knng_last_error(void) { return g_err.c_str(); }
 
-knng_status knng_ctx_create(int num_devices, knng_ctx** out) {
+knng_status knng_ctx_create_on(const int* devices, int num_devices, knng_ctx** out) {
   return guard([&] {
-    require(out != nullptr, "knng_ctx_create: null output");
+    require(out != nullptr && devices != nullptr && num_devices > 0,
+            "knng_ctx_create_on: null argument");
     int count = 0;
     KNNG_CUDA(cudaGetDeviceCount(&count));
     require(count > 0, "knng_ctx_create: no CUDA device");
-    if (num_devices <= 0 || num_devices > count) num_devices = count;
     auto ctx = std::make_unique<knng_ctx>();
-    for (int d = 0; d < num_devices; ++d) {
-      ctx->devices.push_back(d);
-      ctx->runners.push_back(std::make_unique<Runner>(d));
+    for (int i = 0; i < num_devices; ++i) {
+      require(devices[i] >= 0 && devices[i] < count, "knng_ctx_create_on: device out of range");
+      ctx->devices.push_back(devices[i]);
+      ctx->runners.push_back(std::make_unique<Runner>(devices[i]));
     }
-    // NVLink peer access between every pair (pool memory included)
-    for (int a = 0; a < num_devices; ++a) {
+    // NVLink peer access between every pair of the context's devices
+    for (int ia = 0; ia < num_devices; ++ia) {
+      const int a = devices[ia];
       DeviceGuard g(a);
-      for (int b = 0; b < num_devices; ++b) {
+      for (int ib = 0; ib < num_devices; ++ib) {
+        const int b = devices[ib];
         if (a == b) continue;
         int ok = 0;
         KNNG_CUDA(cudaDeviceCanAccessPeer(&ok, a, b));
@@ -311,6 +314,18 @@ knng_status knng_ctx_create(int num_devices, knng_ctx** out) {
     }
     *out = ctx.release();
   });
+}
+
+knng_status knng_ctx_create(int num_devices, knng_ctx** out) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count <= 0) {
+    cudaGetLastError();
+    return guard([&] { throw CudaError("knng_ctx_create: no CUDA device"); });
+  }
+  if (num_devices <= 0 || num_devices > count) num_devices = count;
+  std::vector<int> devs(num_devices);
+  for (int d = 0; d < num_devices; ++d) devs[d] = d;
+  return knng_ctx_create_on(devs.data(), num_devices, out);
 }
 
 void knng_ctx_destroy(knng_ctx* ctx) { delete ctx; }

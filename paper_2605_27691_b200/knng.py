@@ -125,6 +125,7 @@ _vp = C.c_void_p
 _u64 = C.c_uint64
 _SIGS = {
     "knng_abi_version": (C.c_int, []),
+    "knng_ctx_create_on": (C.c_int, [_vp, C.c_int, _vp]),
     "knng_kernel_launches": (C.c_uint64, []),
     "knng_last_error": (C.c_char_p, []),
     "knng_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
@@ -210,9 +211,13 @@ def _check(rc: int):
 
 
 class Context:
-    def __init__(self, num_devices: int = 0):
+    def __init__(self, num_devices: int = 0, devices: Optional[Sequence[int]] = None):
         h = C.c_void_p()
-        _check(lib().knng_ctx_create(num_devices, C.byref(h)))
+        if devices is not None:
+            arr = (C.c_int * len(devices))(*devices)
+            _check(lib().knng_ctx_create_on(arr, len(devices), C.byref(h)))
+        else:
+            _check(lib().knng_ctx_create(num_devices, C.byref(h)))
         self.h = h
 
     def __del__(self):
@@ -238,10 +243,12 @@ class Context:
 _CTX: Optional[Context] = None
 
 
-def context() -> Context:
+def context(devices: Optional[Sequence[int]] = None) -> Context:
+    """The process-wide context (created on first use: every visible GPU, or
+    `devices` -- e.g. a torchrun rank's own GPU)."""
     global _CTX
     if _CTX is None:
-        _CTX = Context(0)
+        _CTX = Context(0, devices)
     return _CTX
 
 
