@@ -320,7 +320,8 @@ def main():
         step(x_dev)
         torch.cuda.synchronize()
         ramp.append(time.perf_counter() - t)
-        if len(ramp) >= 3 and max(ramp[-3:]) <= 1.02 * min(ramp[-3:]):
+        # at least 8 builds: a process's builds 4-7 were still seen to vary
+        if len(ramp) >= 8 and max(ramp[-3:]) <= 1.02 * min(ramp[-3:]):
             break
     for _ in range(args.warmup):
         step(x_dev)
@@ -340,9 +341,11 @@ def main():
             ev[0].record(stream)
             step_ev[0].record(stream)
         for i in range(args.steps):
-            st = knng.NnDescentStats()
+            # per-stage statistics (CUDA events per stage) on the last step only
+            st = knng.NnDescentStats() if i == args.steps - 1 else None
             res = step(x_dev, st if ngpu == 1 else None)
-            stats_list.append(st)
+            if st is not None:
+                stats_list.append(st)
             with torch.cuda.stream(stream):
                 step_ev[i + 1].record(stream)
         with torch.cuda.stream(stream):
@@ -519,7 +522,7 @@ def run_multi(args, ws, rank, dist):
         torch.cuda.synchronize()
         el, = allreduce(dist, [time.perf_counter() - t])
         ramp.append(el)
-        stop = (len(ramp) >= 3 and max(ramp[-3:]) <= 1.02 * min(ramp[-3:])) or \
+        stop = (len(ramp) >= 8 and max(ramp[-3:]) <= 1.02 * min(ramp[-3:])) or \
             time.time() - t_ramp > 60
         stop, = allreduce(dist, [1.0 if stop else 0.0])
         if stop:

@@ -143,7 +143,10 @@ struct DevData {
   DBuf<float> own;
   const float* p = nullptr;
 };
-void stage(Runner& r, const knng_dataset* ds, DevData& out) {
+// slot: which runner scratch receives a host f32 dataset (a call staging two
+// datasets uses 0 and 1); reused across calls, so repeated calls do not
+// re-allocate hundreds of MB each time.
+void stage(Runner& r, const knng_dataset* ds, DevData& out, int slot = 0) {
   check_ds(ds);
   if (ds->elem_kind == KNNG_ELEM_U8) {
     const u64 cells = ds->n * ds->dims;
@@ -166,11 +169,12 @@ void stage(Runner& r, const knng_dataset* ds, DevData& out) {
     out.p = static_cast<const float*>(ds->data);
     return;
   }
-  out.own.alloc(r, ds->n * ds->dims);
+  float* dst = static_cast<float*>(
+      r.scratch(slot ? Runner::kScrStage1 : Runner::kScrStage0, ds->n * ds->dims * 4 + 16));
   if (ds->n)
-    KNNG_CUDA(cudaMemcpyAsync(out.own.p, ds->data, ds->n * ds->dims * 4, cudaMemcpyHostToDevice,
+    KNNG_CUDA(cudaMemcpyAsync(dst, ds->data, ds->n * ds->dims * 4, cudaMemcpyHostToDevice,
                               r.stream));
-  out.p = out.own.p;
+  out.p = dst;
 }
 
 template <class T>
@@ -583,8 +587,8 @@ knng_status knng_ann_search(knng_ctx* ctx, int device, const knng_dataset* queri
     SearchParamsDev sp = to_sp(params);
     validate_search(queries->dims, vectors->dims, sg_n, vectors->n, sp);
     DevData q, v;
-    stage(r, queries, q);
-    stage(r, vectors, v);
+    stage(r, queries, q, 0);
+    stage(r, vectors, v, 1);
     const u64 nq = queries->n;
     // the search graph: device if out_mem is device, else host
     DBuf<u32> sgd;
@@ -653,7 +657,7 @@ knng_status knng_search_throughput_probe(knng_ctx* ctx, int device,
               "ann_search: query/vector datasets incompatible");
       validate_search(queries->dims, c.vectors->dims, c.sg_n, c.vectors->n, sp);
       DevData v;
-      stage(r, c.vectors, v);
+      stage(r, c.vectors, v, 1);
       DBuf<u32> sgd;
       const u32* sg = c.sg_ids;
       if (c.sg_mem != KNNG_MEM_DEVICE) {

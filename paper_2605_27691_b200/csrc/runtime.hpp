@@ -125,7 +125,14 @@ struct Runner {
   // Per-iteration temporaries come from here: allocating and freeing them
   // every iteration occasionally made the host wait on pool growth while
   // the GPU idled (up to ~55 ms, seen with KNNG_TRACE_SLOW).
-  enum ScratchSlot { kScrScan = 0, kScrRadixHist, kScrRadixBase, kScrCount };
+  enum ScratchSlot {
+    kScrScan = 0,
+    kScrRadixHist,
+    kScrRadixBase,
+    kScrStage0,  // host datasets staged by a C-ABI call (two per call at most)
+    kScrStage1,
+    kScrCount
+  };
   void* scratch(int slot, size_t bytes) const {
     if (scratch_.size() < (size_t)kScrCount) scratch_.resize(kScrCount, {nullptr, 0});
     auto& sc = scratch_[slot];
