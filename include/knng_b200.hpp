@@ -608,6 +608,25 @@ inline double recall_at_k(const KnnGraph& test, const GroundTruth& gt, std::size
   return recall_at_k(test, gt.graph, k_eval);
 }
 
+// distance_threshold_recall evalio.cpp:199-215 (host, measurement only): per
+// row, the share of the first k_eval test distances <= the reference row's
+// k_eval-th distance, averaged in row order.
+inline double distance_threshold_recall(const KnnGraph& test, const KnnGraph& reference,
+                                        std::size_t k_eval) {
+  if (k_eval == 0 || k_eval > test.k || k_eval > reference.k)
+    throw std::invalid_argument("distance_threshold_recall: k_eval out of range");
+  if (test.num_sources != reference.num_sources)
+    throw std::invalid_argument("distance_threshold_recall: graphs not comparable");
+  double total = 0.0;
+  for (std::size_t r = 0; r < test.num_sources; ++r) {
+    const float thr = reference.dists[r * reference.k + k_eval - 1];
+    std::size_t c = 0;
+    while (c < test.k && test.dists[r * test.k + c] <= thr) ++c;
+    total += static_cast<double>(std::min(c, k_eval)) / static_cast<double>(k_eval);
+  }
+  return total / static_cast<double>(test.num_sources);
+}
+
 inline void save_graph(const KnnGraph& g, const std::filesystem::path& path) {
   KnnGraph copy = g;
   knng_graph gv = copy.view();

@@ -77,6 +77,8 @@ class Oracle:
         L.ko_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
         L.ko_l2_f32.restype = C.c_float
         L.ko_l2_f32.argtypes = [f32p, f32p, sz]
+        L.ko_cosine_f32.restype = C.c_float
+        L.ko_cosine_f32.argtypes = [f32p, f32p, sz]
         L.ko_gen_random_dataset.argtypes = [sz, sz, C.c_int, C.c_uint64, sz, f32p]
         L.ko_init_random_graph.argtypes = [C.POINTER(KoDataset), sz, C.c_uint64, u32p, f32p, u8p]
         L.ko_sample_neighbors.restype = sz
@@ -111,6 +113,10 @@ class Oracle:
         return self.L.ko_l2_f32(np.ascontiguousarray(a, np.float32),
                                 np.ascontiguousarray(b, np.float32), len(a))
 
+    def cosine(self, a, b):
+        return self.L.ko_cosine_f32(np.ascontiguousarray(a, np.float32),
+                                    np.ascontiguousarray(b, np.float32), len(a))
+
     def gen_random_dataset(self, n, dims, dist, seed, clusters=0):
         out = np.empty((n, dims), np.float32)
         rc = self.L.ko_gen_random_dataset(n, dims, DIST[dist], seed, clusters, out)
@@ -118,12 +124,12 @@ class Oracle:
             raise ValueError("gen_random_dataset: invalid arguments")
         return out
 
-    def init_random_graph(self, x, k, seed):
+    def init_random_graph(self, x, k, seed, metric=0):
         n = x.shape[0]
         ids = np.empty((n, k), np.uint32)
         d = np.empty((n, k), np.float32)
         f = np.empty((n, k), np.uint8)
-        ds = _ds(x)
+        ds = _ds(x, metric)
         if self.L.ko_init_random_graph(C.byref(ds), k, seed, ids, d, f):
             raise ValueError("init_random_graph: need 1 <= k < N")
         return ids, d, f
@@ -144,24 +150,24 @@ class Oracle:
         return dict(bound=b, flags=flags, new_fwd=(nf, cnt[0]), old_fwd=(of, cnt[1]),
                     new_rev=(nr, cnt[2]), old_rev=(orv, cnt[3]))
 
-    def nn_descent(self, x, k, delta=1e-4, rho=0.5, max_iters=100, cap=0, seed=0):
+    def nn_descent(self, x, k, delta=1e-4, rho=0.5, max_iters=100, cap=0, seed=0, metric=0):
         n = x.shape[0]
         ids = np.empty((n, k), np.uint32)
         d = np.empty((n, k), np.float32)
         f = np.empty((n, k), np.uint8)
         acc = np.zeros(max(max_iters, 1), np.uint64)
         p = KoNndParams(k, delta, rho, max_iters, cap, seed)
-        ds = _ds(x)
+        ds = _ds(x, metric)
         it = self.L.ko_nn_descent(C.byref(ds), C.byref(p), ids, d, f, acc)
         if it < 0:
             raise ValueError("nn_descent: invalid arguments")
         return ids, d, f, acc[:it].copy()
 
-    def optimize_graph(self, ids, dists, x, out_degree):
+    def optimize_graph(self, ids, dists, x, out_degree, metric=0):
         n, k = ids.shape
         od = out_degree or k
         sg = np.empty((n, od), np.uint32)
-        ds = _ds(x)
+        ds = _ds(x, metric)
         if self.L.ko_optimize_graph(np.ascontiguousarray(ids, np.uint32),
                                     np.ascontiguousarray(dists, np.float32), n, k,
                                     C.byref(ds), out_degree, sg):
@@ -169,7 +175,7 @@ class Oracle:
         return sg
 
     def ann_search(self, q, sg, v, k_s=10, beam_width=64, num_entry_points=16, max_hops=0,
-                   seed=0):
+                   seed=0, metric=0):
         nq = q.shape[0]
         sg = np.ascontiguousarray(sg, np.uint32)
         n, deg = sg.shape if sg.ndim == 2 else (v.shape[0], 0)
@@ -178,7 +184,7 @@ class Oracle:
         hops = np.empty(nq, np.uint32)
         scored = np.empty(nq, np.uint32)
         p = KoSearchParams(k_s, beam_width, num_entry_points, max_hops, seed)
-        qd, vd = _ds(q), _ds(v)
+        qd, vd = _ds(q, metric), _ds(v, metric)
         sgf = sg.reshape(-1) if sg.size else np.zeros(1, np.uint32)
         if self.L.ko_ann_search(C.byref(qd), sgf, v.shape[0], deg, C.byref(vd), C.byref(p),
                                 ids, d, hops, scored):
@@ -246,11 +252,11 @@ class Oracle:
                                         oi, od)
         return oi, od
 
-    def brute_force_rows(self, x, rows, k):
+    def brute_force_rows(self, x, rows, k, metric=0):
         rows = np.ascontiguousarray(rows, np.uint64)
         ids = np.empty((len(rows), k), np.uint32)
         d = np.empty((len(rows), k), np.float32)
-        ds = _ds(x)
+        ds = _ds(x, metric)
         if self.L.ko_brute_force_rows(C.byref(ds), rows, len(rows), k, ids, d):
             raise ValueError("brute_force_knng: k must be < N")
         return ids, d
@@ -292,6 +298,9 @@ class Ref:
                                             C.c_uint64, f32p]
         L.kr_l2.restype = C.c_float
         L.kr_l2.argtypes = [f32p, f32p, C.c_uint64]
+        L.kr_cosine.restype = C.c_float
+        L.kr_cosine.argtypes = [f32p, f32p, C.c_uint64]
+        L.kr_set_metric.argtypes = [C.c_int]
         L.kr_init_random_graph.argtypes = [f32p, C.c_uint64, C.c_uint64, C.c_uint64,
                                            C.c_uint64, u32p, f32p, u8p]
         L.kr_sample_neighbors.argtypes = [u32p, f32p, u8p, C.c_uint64, C.c_uint64, C.c_double,
@@ -402,6 +411,14 @@ class Ref:
         self._chk(self.L.kr_partition(x, n, dm, ranks, seed, te, off,
                                       loc.ctypes.data if gather else None))
         return (te, off, loc) if gather else (te, off)
+
+    def set_metric(self, metric):
+        """Metric of every dataset the shims build afterwards (0 l2, 1 cosine)."""
+        self.L.kr_set_metric(metric)
+
+    def cosine(self, a, b):
+        return self.L.kr_cosine(np.ascontiguousarray(a, np.float32),
+                                np.ascontiguousarray(b, np.float32), len(a))
 
     def merge_rows(self, a_ids, a_d, b_ids, b_d, k):
         oi = np.empty(k, np.uint32)

@@ -49,8 +49,11 @@ int guard(F&& f) {
   }
 }
 
+// Metric of every dataset the shims build (kr_set_metric; default l2).
+MetricKind g_metric = MetricKind::l2;
+
 Dataset make_ds(const float* data, std::size_t n, std::size_t dims) {
-  Dataset d = Dataset::empty(dims, ElemKind::f32, MetricKind::l2);
+  Dataset d = Dataset::empty(dims, ElemKind::f32, g_metric);
   d.num_points = n;
   d.f32.assign(data, data + n * dims);
   return d;
@@ -124,6 +127,12 @@ int kr_gen_random_dataset(std::uint64_t n, std::uint64_t dims, int dist,
     const Dataset d = gen_random_dataset(n, dims, dd, seed, clusters);
     std::copy(d.f32.begin(), d.f32.end(), out);
   });
+}
+
+void kr_set_metric(int metric) { g_metric = metric ? MetricKind::cosine : MetricKind::l2; }
+
+float kr_cosine(const float* a, const float* b, std::uint64_t d) {
+  return distance(MetricKind::cosine, std::span<const float>(a, d), std::span<const float>(b, d));
 }
 
 float kr_l2(const float* a, const float* b, std::uint64_t d) {

@@ -26,10 +26,12 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+template <bool kCos>
 __global__ __launch_bounds__(kBfThreads) void k_bruteforce(const float* __restrict__ X, u64 n,
                                                            int d, const u64* __restrict__ rows,
                                                            u64 q, u32 k, u32* __restrict__ out_ids,
-                                                           float* __restrict__ out_d) {
+                                                           float* __restrict__ out_d,
+                                                           const float* __restrict__ nrm) {
   __shared__ __align__(16) float s_q[kBfQ * kBfDCP];
   __shared__ __align__(16) float s_x[kBfT * kBfDCP];
   __shared__ u64 s_dm[kBfQ][kBfT];
@@ -88,15 +90,15 @@ __global__ __launch_bounds__(kBfThreads) void k_bruteforce(const float* __restri
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const float4 b = *reinterpret_cast<const float4*>(rb[c] + dd);
-          acc[0][c] = sq_step4(acc[0][c], a0, b);
-          acc[1][c] = sq_step4(acc[1][c], a1, b);
+          acc[0][c] = m_step4<kCos>(acc[0][c], a0, b);
+          acc[1][c] = m_step4<kCos>(acc[1][c], a1, b);
         }
       }
       for (int dd = dc4; dd < dc; ++dd) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          acc[0][c] = sq_step(acc[0][c], ra0[dd], rb[c][dd]);
-          acc[1][c] = sq_step(acc[1][c], ra1[dd], rb[c][dd]);
+          acc[0][c] = m_step<kCos>(acc[0][c], ra0[dd], rb[c][dd]);
+          acc[1][c] = m_step<kCos>(acc[1][c], ra1[dd], rb[c][dd]);
         }
       }
     }
@@ -108,7 +110,10 @@ __global__ __launch_bounds__(kBfThreads) void k_bruteforce(const float* __restri
         const int xi = xb + 16 * c;
         const u64 row = t0 + xi;
         u64 key = kEmptyKey;
-        if (xi < nt && qi < nq && row != s_qrow[qi]) key = pack_key(__fsqrt_rn(acc[r][c]), (u32)row);
+        if (xi < nt && qi < nq && row != s_qrow[qi])
+          key = pack_key(m_finish<kCos>(acc[r][c], kCos ? nrm[s_qrow[qi]] : 0.0f,
+                                        kCos ? nrm[row] : 0.0f),
+                         (u32)row);
         s_dm[qi][xi] = key;
       }
     }
@@ -150,16 +155,46 @@ __global__ __launch_bounds__(kBfThreads) void k_bruteforce(const float* __restri
   }
 }
 
+// Per-row norm chain of cosine_t (core.hpp:44-49): na = sum x*x in index
+// order, no FMA.  One thread per row (a one-off O(N d) pass before a build or
+// search; each row's 16-byte loads stay within its own lines).
+__global__ void k_row_norms(const float* __restrict__ X, u64 n, int d, float* __restrict__ out) {
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (u64)gridDim.x * blockDim.x) {
+    const float* x = X + r * (u64)d;
+    float acc = 0.0f;
+    int i = 0;
+    if ((d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0)
+      for (; i < d; i += 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(x + i));
+        acc = dot_step4(acc, v, v);
+      }
+    for (; i < d; ++i) acc = dot_step(acc, x[i], x[i]);
+    out[r] = acc;
+  }
+}
+
 }  // namespace
 
+void row_norms_device(const Runner& r, const float* X, uint64_t n, int d, float* out) {
+  if (!n) return;
+  DeviceGuard guard(r.device);
+  const unsigned g = (unsigned)std::min<u64>(ceil_div<u64>(n, 256), (u64)r.num_sms * 32);
+  k_row_norms<<<g, 256, 0, r.stream>>>(X, n, d, out);
+  KNNG_LAUNCH_CHECK();
+}
+
 void brute_force_rows_device(Runner& r, const float* X, uint64_t n, int d, const uint64_t* rows,
-                             uint64_t q, uint32_t k, uint32_t* out_ids, float* out_d) {
+                             uint64_t q, uint32_t k, uint32_t* out_ids, float* out_d,
+                             const float* nrm) {
   require(k >= 1 && k < n, "brute_force_knng: k must be < N");
   require(k <= 32, "brute_force_knng: the B200 path supports k <= 32");
   if (!q) return;
   DeviceGuard guard(r.device);
-  k_bruteforce<<<(unsigned)ceil_div<u64>(q, kBfQ), kBfThreads, 0, r.stream>>>(X, n, d, rows, q, k,
-                                                                               out_ids, out_d);
+  const unsigned g = (unsigned)ceil_div<u64>(q, kBfQ);
+  if (nrm)
+    k_bruteforce<true><<<g, kBfThreads, 0, r.stream>>>(X, n, d, rows, q, k, out_ids, out_d, nrm);
+  else
+    k_bruteforce<false><<<g, kBfThreads, 0, r.stream>>>(X, n, d, rows, q, k, out_ids, out_d, nrm);
   KNNG_LAUNCH_CHECK();
 }
 

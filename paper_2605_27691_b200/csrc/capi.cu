@@ -123,8 +123,7 @@ void check_ds(const knng_dataset* ds) {
   require(ds != nullptr && (ds->data != nullptr || ds->n == 0), "knng: null dataset");
   require(ds->elem_kind == KNNG_ELEM_F32 || ds->elem_kind == KNNG_ELEM_U8,
           "knng: unknown element kind");
-  require(ds->metric == KNNG_METRIC_L2,
-          "knng: the B200 path implements the l2 metric (cosine is not built yet)");
+  require(ds->metric == KNNG_METRIC_L2 || ds->metric == KNNG_METRIC_COS, "knng: unknown metric");
   require(ds->dims >= 1 && ds->dims <= (1u << 20), "knng: dims out of range");
 }
 
@@ -142,11 +141,25 @@ __global__ void k_u8_to_f32(const uint8_t* __restrict__ in, u64 count, float* __
 struct DevData {
   DBuf<float> own;
   const float* p = nullptr;
+  DBuf<float> nrm_own;  // cosine: per-row norm chains (core.hpp:44-49); else empty
+  const float* nrm = nullptr;
 };
+
+void stage_rows(Runner& r, const knng_dataset* ds, DevData& out, int slot);
+// Stage the rows, then (cosine) their norm chains: every kernel then runs only
+// the per-pair dot chain and finishes with cos_finish (common.cuh).
+void stage(Runner& r, const knng_dataset* ds, DevData& out, int slot = 0) {
+  stage_rows(r, ds, out, slot);
+  if (ds->metric == KNNG_METRIC_COS) {
+    out.nrm_own.alloc(r, ds->n ? ds->n : 1);
+    row_norms_device(r, out.p, ds->n, (int)ds->dims, out.nrm_own.p);
+    out.nrm = out.nrm_own.p;
+  }
+}
 // slot: which runner scratch receives a host f32 dataset (a call staging two
 // datasets uses 0 and 1); reused across calls, so repeated calls do not
 // re-allocate hundreds of MB each time.
-void stage(Runner& r, const knng_dataset* ds, DevData& out, int slot = 0) {
+void stage_rows(Runner& r, const knng_dataset* ds, DevData& out, int slot) {
   check_ds(ds);
   if (ds->elem_kind == KNNG_ELEM_U8) {
     const u64 cells = ds->n * ds->dims;
@@ -256,11 +269,23 @@ void fill_dist_result(const DistResult& d, knng_dist_result* r) {
   r->num_snapshots = d.snap_labels.size();
 }
 
+// row_distance (core.hpp:82-93): l2_exact, or (nrm != null) the cosine dot
+// chain in index order finished with the rows' norm chains.
 __global__ void k_row_dist(const float* __restrict__ X, int d, const u32* __restrict__ i,
-                           const u32* __restrict__ j, u64 count, float* __restrict__ out) {
+                           const u32* __restrict__ j, u64 count, float* __restrict__ out,
+                           const float* __restrict__ nrm) {
   for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < count;
-       t += (u64)gridDim.x * blockDim.x)
-    out[t] = l2_exact(X + (u64)i[t] * d, X + (u64)j[t] * d, d);
+       t += (u64)gridDim.x * blockDim.x) {
+    const float* a = X + (u64)i[t] * d;
+    const float* b = X + (u64)j[t] * d;
+    if (!nrm) {
+      out[t] = l2_exact(a, b, d);
+      continue;
+    }
+    float dot = 0.0f;
+    for (int e = 0; e < d; ++e) dot = dot_step(dot, a[e], b[e]);
+    out[t] = cos_finish(dot, nrm[i[t]], nrm[j[t]]);
+  }
 }
 
 __global__ void k_pack(const u32* __restrict__ ids, const float* __restrict__ dists, u64 count,
@@ -361,7 +386,7 @@ knng_status knng_row_distances(knng_ctx* ctx, int device, const knng_dataset* ds
     copy_in(r, di.p, i, count, false);
     copy_in(r, dj.p, j, count, false);
     k_row_dist<<<grid_for(r, count), 256, 0, r.stream>>>(x.p, (int)ds->dims, di.p, dj.p, count,
-                                                         dout.p);
+                                                         dout.p, x.nrm);
     KNNG_LAUNCH_CHECK();
     copy_out(r, out, dout.p, count, false);
     r.sync();
@@ -409,7 +434,7 @@ knng_status knng_init_random_graph(knng_ctx* ctx, int device, const knng_dataset
     require(k >= 1 && k < ds->n, "init_random_graph: need 1 <= k < N");
     DBuf<u64> keys(r, ds->n * k);
     DBuf<u32> flags(r, ds->n);
-    init_random_graph_device(r, DevRows{x.p, ds->n, (int)ds->dims}, (u32)k, seed, keys.p,
+    init_random_graph_device(r, DevRows{x.p, ds->n, (int)ds->dims, x.nrm}, (u32)k, seed, keys.p,
                              flags.p);
     const bool dev = out->mem == KNNG_MEM_DEVICE;
     DBuf<u32> ti;
@@ -493,7 +518,8 @@ knng_status knng_nn_descent(knng_ctx* ctx, int device, const knng_dataset* ds,
     DBuf<u32> flags(r, n);
     NndStats st;
     tr.mark("alloc");
-    nn_descent_device(r, DevRows{x.p, n, (int)ds->dims}, p, keys.p, flags.p, &st, stats != nullptr,
+    nn_descent_device(r, DevRows{x.p, n, (int)ds->dims, x.nrm}, p, keys.p, flags.p, &st,
+                      stats != nullptr,
                       ctx->workspace(device));
     tr.mark("build");
     const bool dev = out->mem == KNNG_MEM_DEVICE;
@@ -561,10 +587,12 @@ knng_status knng_optimize_graph(knng_ctx* ctx, int device, const knng_graph* gph
     DBuf<u64> keys(r, n * k);
     import_graph_device(r, ids, dd, nullptr, n, (u32)k, keys.p, nullptr);
     if (dev) {
-      optimize_graph_device(r, keys.p, n, (u32)k, 0, x.p, (int)ds->dims, (u32)out_degree, sg_ids);
+      optimize_graph_device(r, keys.p, n, (u32)k, 0, x.p, (int)ds->dims, (u32)out_degree, sg_ids,
+                            nullptr, x.nrm);
     } else {
       DBuf<u32> sg(r, n * out_degree);
-      optimize_graph_device(r, keys.p, n, (u32)k, 0, x.p, (int)ds->dims, (u32)out_degree, sg.p);
+      optimize_graph_device(r, keys.p, n, (u32)k, 0, x.p, (int)ds->dims, (u32)out_degree, sg.p,
+                            nullptr, x.nrm);
       copy_out(r, sg_ids, sg.p, n * out_degree, false);
       r.sync();
     }
@@ -602,12 +630,13 @@ knng_status knng_ann_search(knng_ctx* ctx, int device, const knng_dataset* queri
     const u64 ks = sp.k_s;
     if (out_mem == KNNG_MEM_DEVICE) {
       ann_search_device(r, q.p, nq, (int)queries->dims, sg, (u32)degree, v.p, vectors->n, sp, 0,
-                        out_ids, out_dists, hops, scored, nullptr);
+                        out_ids, out_dists, hops, scored, nullptr, 0, q.nrm, v.nrm);
     } else {
       DBuf<u32> oi(r, nq * ks), hh(r, hops ? nq : 0), ss(r, scored ? nq : 0);
       DBuf<float> od(r, nq * ks);
       ann_search_device(r, q.p, nq, (int)queries->dims, sg, (u32)degree, v.p, vectors->n, sp, 0,
-                        oi.p, od.p, hops ? hh.p : nullptr, scored ? ss.p : nullptr, nullptr);
+                        oi.p, od.p, hops ? hh.p : nullptr, scored ? ss.p : nullptr, nullptr, 0,
+                        q.nrm, v.nrm);
       copy_out(r, out_ids, oi.p, nq * ks, false);
       copy_out(r, out_dists, od.p, nq * ks, false);
       if (hops) copy_out(r, hops, hh.p, nq, false);
@@ -668,7 +697,7 @@ knng_status knng_search_throughput_probe(knng_ctx* ctx, int device,
       r.sync();
       KNNG_CUDA(cudaEventRecord(e0, r.stream));
       ann_search_device(r, q.p, nq, (int)queries->dims, sg, (u32)c.degree, v.p, c.vectors->n, sp,
-                        0, oi.p, od.p, nullptr, nullptr, nullptr);
+                        0, oi.p, od.p, nullptr, nullptr, nullptr, 0, q.nrm, v.nrm);
       KNNG_CUDA(cudaEventRecord(e1, r.stream));
       KNNG_CUDA(cudaEventSynchronize(e1));
       float ms = 0;
@@ -785,6 +814,7 @@ knng_status knng_build_distributed(knng_ctx* ctx, const knng_dataset* ds,
     require(ctx && ds && cfg && out, "build_distributed: null argument");
     check_ds(ds);
     RefineCfg c = to_cfg(cfg);
+    c.cosine = ds->metric == KNNG_METRIC_COS;
     require(out->n == ds->n && out->k == c.k, "build_distributed: output shape mismatch");
     DistResult res;
     const float* xp = static_cast<const float*>(ds->data);
@@ -824,6 +854,7 @@ knng_status knng_build_distributed_rank(knng_ctx* ctx, int device, uint64_t rank
     check_ds(ds);
     RefineCfg c = to_cfg(cfg);
     c.ranks = world_size;
+    c.cosine = ds->metric == KNNG_METRIC_COS;
     HostTransport t;
     t.user = user;
     t.allgather = allgather;
@@ -891,11 +922,12 @@ knng_status knng_brute_force(knng_ctx* ctx, int device, const knng_dataset* ds,
     DBuf<u64> rw(r, q + 1);
     copy_in(r, rw.p, rows, q, false);
     if (out_mem == KNNG_MEM_DEVICE) {
-      brute_force_rows_device(r, x.p, ds->n, (int)ds->dims, rw.p, q, (u32)k, out_ids, out_dists);
+      brute_force_rows_device(r, x.p, ds->n, (int)ds->dims, rw.p, q, (u32)k, out_ids, out_dists,
+                              x.nrm);
     } else {
       DBuf<u32> oi(r, q * k);
       DBuf<float> od(r, q * k);
-      brute_force_rows_device(r, x.p, ds->n, (int)ds->dims, rw.p, q, (u32)k, oi.p, od.p);
+      brute_force_rows_device(r, x.p, ds->n, (int)ds->dims, rw.p, q, (u32)k, oi.p, od.p, x.nrm);
       copy_out(r, out_ids, oi.p, q * k, false);
       copy_out(r, out_dists, od.p, q * k, false);
       r.sync();

@@ -131,6 +131,49 @@ __device__ __forceinline__ float sq_step4(float acc, float4 a, float4 b) {
   return sq_step2(acc, a.z, a.w, b.z, b.w);
 }
 
+// ---------------------------------------------------------------------------
+// cosine (core.hpp:41-55): dot, na and nb are three independent sequential
+// chains.  A row's norm chain does not depend on its partner, so it is
+// computed once per row (row_norms_device) and only the dot runs per pair;
+// the finish repeats the reference's operations in order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float dot_step(float acc, float a, float b) {
+  return __fadd_rn(acc, __fmul_rn(a, b));
+}
+__device__ __forceinline__ float dot_step2(float acc, float a0, float a1, float b0, float b1) {
+  unsigned long long A, B, T;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(A) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(T) : "l"(A), "l"(B));
+  float s0, s1;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(s0), "=f"(s1) : "l"(T));
+  return __fadd_rn(__fadd_rn(acc, s0), s1);
+}
+__device__ __forceinline__ float dot_step4(float acc, float4 a, float4 b) {
+  acc = dot_step2(acc, a.x, a.y, b.x, b.y);
+  return dot_step2(acc, a.z, a.w, b.z, b.w);
+}
+__device__ __forceinline__ float cos_finish(float dot, float na, float nb) {
+  if (na == 0.0f || nb == 0.0f) return 1.0f;
+  const float v = __fsub_rn(1.0f, __fdiv_rn(dot, __fmul_rn(__fsqrt_rn(na), __fsqrt_rn(nb))));
+  return v < 0.0f ? 0.0f : v;
+}
+
+// Metric-generic steps: kCos selects the dot chain, else the L2 chain.
+template <bool kCos>
+__device__ __forceinline__ float m_step4(float acc, float4 a, float4 b) {
+  return kCos ? dot_step4(acc, a, b) : sq_step4(acc, a, b);
+}
+template <bool kCos>
+__device__ __forceinline__ float m_step(float acc, float a, float b) {
+  return kCos ? dot_step(acc, a, b) : sq_step(acc, a, b);
+}
+// Distance from a finished accumulator; na/nb (row norm chains) read only for cosine.
+template <bool kCos>
+__device__ __forceinline__ float m_finish(float acc, float na, float nb) {
+  return kCos ? cos_finish(acc, na, nb) : __fsqrt_rn(acc);
+}
+
 // Full exact distance between two global/shared rows.
 __device__ __forceinline__ float l2_exact(const float* __restrict__ a,
                                           const float* __restrict__ b, int d) {

@@ -32,12 +32,14 @@ struct PruneArgs {
   u32 k;
   u32 id_base;  // ids in keys are (local id + id_base)
   const float* X;
+  const float* nrm;  // cosine norm chains of X's rows (null: l2)
   int d;
   int DC, DCP;
   u32* kept;   // n bitmasks
   u32* rcnt;   // n reverse-edge counts
 };
 
+template <bool kCos>
 __global__ __launch_bounds__(kPruneThreads) void k_prune(PruneArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   u32* s_ids = reinterpret_cast<u32*>(smem);          // 32
@@ -100,13 +102,13 @@ __global__ __launch_bounds__(kPruneThreads) void k_prune(PruneArgs a) {
 #pragma unroll
           for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[r][c] = sq_step4(acc[r][c], va[r], vb[c]);
+            for (int c = 0; c < 4; ++c) acc[r][c] = m_step4<kCos>(acc[r][c], va[r], vb[c]);
         }
         for (int dd = dc4; dd < dc; ++dd) {
 #pragma unroll
           for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[r][c] = sq_step(acc[r][c], ra[r][dd], rb[c][dd]);
+            for (int c = 0; c < 4; ++c) acc[r][c] = m_step<kCos>(acc[r][c], ra[r][dd], rb[c][dd]);
         }
       }
     }
@@ -118,7 +120,10 @@ __global__ __launch_bounds__(kPruneThreads) void k_prune(PruneArgs a) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int j = tj + RT * c;
-          if (i < j && j < k && __fsqrt_rn(acc[r][c]) < s_d[j]) atomicOr(&s_det[j], 1u << i);
+          if (i < j && j < k &&
+              m_finish<kCos>(acc[r][c], kCos ? __ldg(a.nrm + s_ids[i]) : 0.0f,
+                             kCos ? __ldg(a.nrm + s_ids[j]) : 0.0f) < s_d[j])
+            atomicOr(&s_det[j], 1u << i);
         }
       }
     }
@@ -228,7 +233,7 @@ unsigned warp_grid(const Runner& r, u64 items) {
 
 void optimize_graph_device(Runner& r, const uint64_t* keys, uint64_t n, uint32_t k,
                            uint32_t id_base, const float* X, int d, uint32_t out_degree,
-                           uint32_t* sg, uint64_t* launches) {
+                           uint32_t* sg, uint64_t* launches, const float* nrm) {
   if (out_degree == 0) out_degree = k;
   require(out_degree <= k, "optimize_graph: out_degree must be <= k");
   require(k >= 1 && k <= 32, "optimize_graph: the B200 path supports 1 <= k <= 32");
@@ -243,6 +248,7 @@ void optimize_graph_device(Runner& r, const uint64_t* keys, uint64_t n, uint32_t
   a.k = k;
   a.id_base = id_base;
   a.X = X;
+  a.nrm = nrm;
   a.d = d;
   a.DC = d <= 128 ? ((d + 7) & ~7) : 128;
   a.DCP = a.DC + 4;
@@ -250,12 +256,18 @@ void optimize_graph_device(Runner& r, const uint64_t* keys, uint64_t n, uint32_t
   a.rcnt = rcnt.p;
   const int rows = ((int)k + 3) & ~3;
   const size_t smem = 384 + (size_t)rows * a.DCP * 4;
-  KNNG_CUDA(cudaFuncSetAttribute(k_prune, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  KNNG_CUDA(cudaFuncSetAttribute(k_prune<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  KNNG_CUDA(cudaFuncSetAttribute(k_prune<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
   int per_sm = 0;
-  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prune, kPruneThreads, smem));
+  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prune<false>, kPruneThreads,
+                                                          smem));
   if (per_sm < 1) per_sm = 1;
-  k_prune<<<persistent_grid(r, per_sm, n), kPruneThreads, smem, r.stream>>>(a);
+  if (nrm)
+    k_prune<true><<<persistent_grid(r, per_sm, n), kPruneThreads, smem, r.stream>>>(a);
+  else
+    k_prune<false><<<persistent_grid(r, per_sm, n), kPruneThreads, smem, r.stream>>>(a);
   KNNG_LAUNCH_CHECK();
   exclusive_scan_u32(r, rcnt.p, roff.p, n);
   uint64_t total = 0;

@@ -12,6 +12,7 @@ namespace knng_b200 {
 // ids (local) to sg.
 void optimize_graph_device(Runner& r, const uint64_t* keys, uint64_t n, uint32_t k,
                            uint32_t id_base, const float* X, int d, uint32_t out_degree,
-                           uint32_t* sg, uint64_t* launches = nullptr);
+                           uint32_t* sg, uint64_t* launches = nullptr,
+                           const float* nrm = nullptr);  // nrm: cosine norm chains
 
 }  // namespace knng_b200

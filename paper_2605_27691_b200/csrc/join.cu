@@ -215,6 +215,7 @@ __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
 // ---------------------------------------------------------------------------
 struct JoinArgs {
   const float* X;
+  const float* nrm;  // cosine norm chains (null: l2)
   int d;
   const u32* L_ids;
   const u32* L_cnt;
@@ -477,6 +478,7 @@ __device__ __forceinline__ Tile decode_tile(const Smem& s, int q, int t) {
   return T;
 }
 
+template <bool kCos>
 __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Smem s = carve(smem, a.RMAX, a.RB, a.DCP);
@@ -562,13 +564,14 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
 #pragma unroll
           for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[t][r][c] = sq_step4(acc[t][r][c], va[r], vb[c]);
+            for (int c = 0; c < 4; ++c) acc[t][r][c] = m_step4<kCos>(acc[t][r][c], va[r], vb[c]);
         }
         for (int dd = dc4; dd < dc; ++dd) {
 #pragma unroll
           for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[t][r][c] = sq_step(acc[t][r][c], ra[r][dd], rb[c][dd]);
+            for (int c = 0; c < 4; ++c)
+              acc[t][r][c] = m_step<kCos>(acc[t][r][c], ra[r][dd], rb[c][dd]);
         }
       }
     }
@@ -598,7 +601,10 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
               jl = T[t].nn + jj;
             }
             if (!valid) continue;
-            const float dist = __fsqrt_rn(acc[t][r][c]);
+            const float dist =
+                kCos ? cos_finish(acc[t][r][c], __ldg(a.nrm + s.ids(m)[lb + i]),
+                                  __ldg(a.nrm + s.ids(m)[lb + jl]))
+                     : __fsqrt_rn(acc[t][r][c]);
             acc[t][r][c] = dist;
             ++my_pairs;
             const int bit = (r * 4 + c) * 2;
@@ -726,10 +732,12 @@ JoinPlan plan_join(const Runner& r, int d, uint32_t k, uint32_t B) {
   require(rb >= max_rows, "nn_descent: feature rows too wide for the join's smem batches");
   p.RB = rb;
   p.smem = join_smem_bytes(p.RMAX, p.RB, p.DCP);
-  KNNG_CUDA(cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  KNNG_CUDA(cudaFuncSetAttribute(k_join<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)p.smem));
+  KNNG_CUDA(cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)p.smem));
   int per_sm = 0;
-  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_join, kJT, p.smem));
+  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_join<false>, kJT, p.smem));
   p.grid = (unsigned)r.num_sms * (unsigned)std::max(per_sm, 1);
   const uint64_t nn_max = 2ull * B, no_max = (uint64_t)k + B;
   const uint64_t max_offers_pp = 2 * (nn_max * (nn_max - 1) / 2 + nn_max * no_max);
@@ -760,6 +768,7 @@ void build_active_list(const Runner& r, uint64_t n, const uint32_t* L_cnt, uint3
 void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& l) {
   JoinArgs a{};
   a.X = l.X;
+  a.nrm = l.nrm;
   a.d = l.d;
   a.L_ids = l.L_ids;
   a.L_cnt = l.L_cnt;
@@ -778,7 +787,10 @@ void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& l) {
   a.DCP = plan.DCP;
   a.RB = plan.RB;
   a.counters = l.counters;
-  k_join<<<plan.grid, kJT, plan.smem, r.stream>>>(a);
+  if (a.nrm)
+    k_join<true><<<plan.grid, kJT, plan.smem, r.stream>>>(a);
+  else
+    k_join<false><<<plan.grid, kJT, plan.smem, r.stream>>>(a);
   KNNG_LAUNCH_CHECK();
 }
 

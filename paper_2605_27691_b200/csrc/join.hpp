@@ -33,6 +33,7 @@ void launch_join_lists(const Runner& r, uint64_t n, uint32_t k, uint32_t B, int 
 
 struct JoinLaunch {
   const float* X = nullptr;
+  const float* nrm = nullptr;  // cosine norm chains (null: l2)
   int d = 0;
   const uint32_t* L_ids = nullptr;
   const uint32_t* L_cnt = nullptr;

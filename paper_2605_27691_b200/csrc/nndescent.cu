@@ -77,10 +77,12 @@ constexpr u32 kInitDims = 64;  // dims per staging round (d % 4 == 0 path)
 
 constexpr int kInitThreads = 128;  // 4 warps: 4 x 8.7 KB staging fits static smem
 
+template <bool kCos>
 __global__ __launch_bounds__(kInitThreads) void k_init(const float* __restrict__ X, u64 n, int d, u32 k,
                                               u64 seed, u64* __restrict__ keys,
                                               u32* __restrict__ flags,
-                                              float* __restrict__ worst) {
+                                              float* __restrict__ worst,
+                                              const float* __restrict__ nrm) {
   // per warp: 32 staged rows x (kInitDims + 4) floats | 32 picks
   __shared__ __align__(16) float s_rows[kInitThreads / 32][32 * (kInitDims + 4)];
   __shared__ u32 s_pick[kInitThreads / 32][32];
@@ -118,17 +120,18 @@ __global__ __launch_bounds__(kInitThreads) void k_init(const float* __restrict__
         if (lane < k) {
           const float* my = st + lane * kStride;
           for (int i = 0; i < cl; i += 4)
-            acc = sq_step4(acc, *reinterpret_cast<const float4*>(xr + c0 + i),
+            acc = m_step4<kCos>(acc, *reinterpret_cast<const float4*>(xr + c0 + i),
                            *reinterpret_cast<const float4*>(my + i));
         }
         __syncwarp();
       }
     } else if (lane < k) {
       const float* xo = X + (u64)my_id * d;
-      for (int i = 0; i < d; ++i) acc = sq_step(acc, xr[i], xo[i]);
+      for (int i = 0; i < d; ++i) acc = m_step<kCos>(acc, xr[i], xo[i]);
     }
     u64 key = kEmptyKey;
-    if (lane < k) key = pack_key(__fsqrt_rn(acc), my_id);
+    if (lane < k)
+      key = pack_key(m_finish<kCos>(acc, kCos ? nrm[r] : 0.0f, kCos ? nrm[my_id] : 0.0f), my_id);
     key = warp_sort32(key);
     if (lane < k) keys[r * k + lane] = key;
     const u64 last = __shfl_sync(kFull, key, k - 1);
@@ -426,15 +429,27 @@ void validate_nnd(const NndParams& p, uint64_t n) {
   require(n < 0xffffffffull, "nn_descent: N must fit a 32-bit point id");
 }
 
+namespace {
+void launch_init(const Runner& r, const DevRows& ds, u32 k, u64 seed, u64* keys, u32* flags,
+                 float* worst) {
+  const unsigned g =
+      (unsigned)std::min<u64>(ceil_div<u64>(ds.n, kInitThreads / 32), (u64)r.num_sms * 32);
+  if (ds.nrm)
+    k_init<true><<<g, kInitThreads, 0, r.stream>>>(ds.x, ds.n, ds.d, k, seed, keys, flags, worst,
+                                                   ds.nrm);
+  else
+    k_init<false><<<g, kInitThreads, 0, r.stream>>>(ds.x, ds.n, ds.d, k, seed, keys, flags, worst,
+                                                    nullptr);
+  KNNG_LAUNCH_CHECK();
+}
+}  // namespace
+
 void init_random_graph_device(Runner& r, const DevRows& ds, uint32_t k, uint64_t seed,
                               uint64_t* keys, uint32_t* flags) {
   require(k >= 1 && k < ds.n, "init_random_graph: need 1 <= k < N");
   require(k <= 32, "init_random_graph: the B200 path supports k <= 32");
   DBuf<float> worst(r, ds.n);
-  k_init<<<(unsigned)std::min<u64>(ceil_div<u64>(ds.n, kInitThreads / 32), (u64)r.num_sms * 32),
-           kInitThreads, 0, r.stream>>>(ds.x, ds.n, ds.d, k, seed, keys, flags,
-                                                   worst.p);
-  KNNG_LAUNCH_CHECK();
+  launch_init(r, ds, k, seed, keys, flags, worst.p);
 }
 
 namespace {
@@ -579,9 +594,7 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   alloc_lists(r, n, k, B, s, c);
   uint64_t launches = 0;
 
-  k_init<<<(unsigned)std::min<u64>(ceil_div<u64>(n, kInitThreads / 32), (u64)r.num_sms * 32),
-           kInitThreads, 0, r.stream>>>(ds.x, n, ds.d, k, p.seed, keys, flags, worst.p);
-  KNNG_LAUNCH_CHECK();
+  launch_init(r, ds, k, p.seed, keys, flags, worst.p);
   ++launches;
   tm.tick(kStInit);
 
@@ -630,6 +643,7 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   JoinLaunch jl;
   jl.act = act.p;
   jl.X = ds.x;
+  jl.nrm = ds.nrm;
   jl.d = ds.d;
   jl.L_ids = L_ids_p;
   jl.L_cnt = L_cnt.p;

@@ -64,6 +64,7 @@ struct DevRows {
   const float* x = nullptr;
   uint64_t n = 0;
   int d = 0;
+  const float* nrm = nullptr;  // cosine norm chains (row_norms_device); null -> l2
 };
 
 void validate_nnd(const NndParams& p, uint64_t n);

@@ -109,6 +109,16 @@ uint64_t effective_groups(const std::vector<uint64_t>& offsets, const RefineCfg&
   return skip ? p : cfg.groups;
 }
 
+// Cosine norm chains of n rows (row_norms_device); empty (p == null -> l2)
+// unless the build runs the cosine metric.
+DBuf<float> norms_of(const Shared& S, Runner& r, const float* x, uint64_t n) {
+  DBuf<float> out;
+  if (!S.cfg->cosine) return out;
+  out.alloc(r, n ? n : 1);
+  row_norms_device(r, x, n, S.d, out.p);
+  return out;
+}
+
 void pull_rows(Shared& S, RankState& R, uint64_t j, const char* name, void* dst) {
   S.world->get(R.rank, j, name, dst, *R.runner);
 }
@@ -120,8 +130,9 @@ void search_and_merge(Shared& S, RankState& R, const u32* sg, const float* vec, 
   Runner& r = *R.runner;
   DBuf<u32> rid(r, R.n_local * S.ks);
   DBuf<float> rd(r, R.n_local * S.ks);
+  const DBuf<float> qn = norms_of(S, r, R.local_x.p, R.n_local), vn = norms_of(S, r, vec, nvec);
   ann_search_device(r, R.local_x.p, R.n_local, S.d, sg, (u32)S.od, vec, nvec, S.sp,
-                    (u32)id_base, rid.p, rd.p, nullptr, nullptr, &R.sc);
+                    (u32)id_base, rid.p, rd.p, nullptr, nullptr, &R.sc, 0, qn.p, vn.p);
   merge_results_device(r, R.keys.p, nullptr, R.n_local, (u32)S.k, rid.p, rd.p, (u32)S.ks, 0);
 }
 
@@ -147,7 +158,11 @@ void tree_level(Shared& S, RankState& R, uint64_t level, DBuf<float>& span_x, ui
     pull_rows(S, R, j, kGraph, pk.p + at * S.k);
   }
   DBuf<u32> sg(r, cnt * S.od);
-  optimize_graph_device(r, pk.p, cnt, (u32)S.k, (u32)base, px.p, S.d, (u32)S.od, sg.p);
+  {
+    const DBuf<float> pn = norms_of(S, r, px.p, cnt);
+    optimize_graph_device(r, pk.p, cnt, (u32)S.k, (u32)base, px.p, S.d, (u32)S.od, sg.p, nullptr,
+                          pn.p);
+  }
   search_and_merge(S, R, sg.p, px.p, cnt, base);
   // accumulate the span dataset in rank order (refine.cpp:216-226)
   DBuf<float> ns(r, (span_n + cnt) * S.d);
@@ -188,7 +203,11 @@ DBuf<u32> grouped_merge(Shared& S, RankState& R, const float* span_x, uint64_t s
       pull_rows(S, R, j, kGraph, dst);
   }
   DBuf<u32> gs(r, cnt * S.od);
-  optimize_graph_device(r, concat.p, cnt, (u32)S.k, (u32)base, span_x, S.d, (u32)S.od, gs.p);
+  {
+    const DBuf<float> sn = norms_of(S, r, span_x, cnt);
+    optimize_graph_device(r, concat.p, cnt, (u32)S.k, (u32)base, span_x, S.d, (u32)S.od, gs.p,
+                          nullptr, sn.p);
+  }
   S.world->publish(R.rank, kSGraph, gs.p, cnt * S.od * 4,
                    wire_region_size(RegionKind::sgraph, cnt, S.od), r);
   S.world->barrier(R.rank, r);
@@ -222,8 +241,11 @@ void a2a_refine(Shared& S, RankState& R) {
   Runner& r = *R.runner;
   const uint64_t p = S.offsets.size() - 1;
   DBuf<u32> own(r, R.n_local * S.od);
-  optimize_graph_device(r, R.keys.p, R.n_local, (u32)S.k, (u32)S.offsets[R.rank], R.local_x.p,
-                        S.d, (u32)S.od, own.p);
+  {
+    const DBuf<float> ln = norms_of(S, r, R.local_x.p, R.n_local);
+    optimize_graph_device(r, R.keys.p, R.n_local, (u32)S.k, (u32)S.offsets[R.rank], R.local_x.p,
+                          S.d, (u32)S.od, own.p, nullptr, ln.p);
+  }
   S.world->publish(R.rank, kDataset, R.local_x.p, R.n_local * S.d * 4,
                    wire_region_size(RegionKind::dataset, R.n_local, S.d, S.cfg->u8_elems), r);
   S.world->publish(R.rank, kSGraph, own.p, R.n_local * S.od * 4,
@@ -290,7 +312,8 @@ void local_build_rank(Shared& S, const RefineCfg& cfg, RankState& R) {
   np.k = (uint32_t)cfg.k;
   np.seed = p == 1 ? cfg.nn.seed : mix_seed(cfg.nn.seed, R.rank);  // refine.cpp:385
   DBuf<u32> flags(r, R.n_local);
-  nn_descent_device(r, DevRows{R.local_x.p, R.n_local, S.d}, np, R.keys.p, flags.p, &R.nst,
+  const DBuf<float> ln = norms_of(S, r, R.local_x.p, R.n_local);
+  nn_descent_device(r, DevRows{R.local_x.p, R.n_local, S.d, ln.p}, np, R.keys.p, flags.p, &R.nst,
                     true, R.ws);
   shift_ids_device(r, R.keys.p, R.n_local * S.k, (int64_t)S.offsets[R.rank]);
   r.sync();

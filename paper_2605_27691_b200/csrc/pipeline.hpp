@@ -26,6 +26,7 @@ struct RefineCfg {
   bool capture_snapshots = false;
   uint64_t max_concat_bytes = 0;
   uint64_t seed = 0;
+  bool cosine = false;    // MetricKind::cosine (core.hpp:41-55): kernels run the dot chain
   bool u8_elems = false;  // input rows were u8 (expanded to f32 on the device): wire sizes
                           // and footprint estimates use 1 byte per element
 };

@@ -37,8 +37,13 @@ void translate_rows_device(const Runner& r, const uint64_t* keys, uint64_t rows,
                            float* out_d, uint32_t* out_rows);
 
 // Exact k-NN (brute_force_knng evalio.cpp:125-147) of rows[0..q) against all n
-// rows of X (self excluded), k <= 32; keys out q x k.
+// rows of X (self excluded), k <= 32; keys out q x k.  nrm = the rows' norm
+// chains (row_norms_device) selects the cosine metric; null -> l2.
 void brute_force_rows_device(Runner& r, const float* X, uint64_t n, int d, const uint64_t* rows,
-                             uint64_t q, uint32_t k, uint32_t* out_ids, float* out_d);
+                             uint64_t q, uint32_t k, uint32_t* out_ids, float* out_d,
+                             const float* nrm = nullptr);
+
+// Cosine norm chains (core.hpp:44-49) of rows [0, n) of X into out[n].
+void row_norms_device(const Runner& r, const float* X, uint64_t n, int d, float* out);
 
 }  // namespace knng_b200

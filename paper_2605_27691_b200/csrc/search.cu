@@ -57,6 +57,8 @@ __device__ __forceinline__ void cpa_wait_all() {
 
 struct SearchArgs {
   const float* Q;
+  const float* qn;  // cosine norm chains of Q / V rows (null: l2)
+  const float* vn;
   u64 nq;
   int d;
   const float* V;
@@ -182,9 +184,10 @@ struct Visited {
 // Exact-order L2 distances of the lanes' candidates (take = lane has one):
 // rows are staged chunk by chunk with coalesced cp.async, one row per warp
 // instruction, then each lane sums its row sequentially (l2_exact order).
+template <bool kCos>
 __device__ __forceinline__ u64 score_batch(const SearchArgs& a, const float* __restrict__ s_q,
                                            float* __restrict__ s_stage, u64* __restrict__ s_ptr,
-                                           u32 id, bool take) {
+                                           u32 id, bool take, float qnorm) {
   const unsigned lane = lane_id();
   __syncwarp();  // reconverge after the visited-set CAS loops
   const unsigned fm = __ballot_sync(kFull, take);
@@ -265,16 +268,17 @@ __device__ __forceinline__ u64 score_batch(const SearchArgs& a, const float* __r
       const float* my = s_stage + (ch % nbuf) * buf_floats + rank * a.stride;
       if (a.vec4) {
         for (u32 i = 0; i < cl; i += 4)
-          acc = sq_step4(acc, *reinterpret_cast<const float4*>(qq + i),
-                         *reinterpret_cast<const float4*>(my + i));
+          acc = m_step4<kCos>(acc, *reinterpret_cast<const float4*>(qq + i),
+                              *reinterpret_cast<const float4*>(my + i));
       } else {
-        for (u32 i = 0; i < cl; ++i) acc = sq_step(acc, qq[i], my[i]);
+        for (u32 i = 0; i < cl; ++i) acc = m_step<kCos>(acc, qq[i], my[i]);
       }
     }
     __syncwarp();
     if (ch + nbuf < nch) issue(ch + nbuf, ch % nbuf);
   }
-  return take ? pack_key(__fsqrt_rn(acc), id) : kEmptyKey;
+  if (!take) return kEmptyKey;
+  return pack_key(m_finish<kCos>(acc, qnorm, kCos ? __ldg(a.vn + id) : 0.0f), id);
 }
 
 // Merge the lane-held candidate keys (kEmptyKey = none) into the sorted
@@ -371,6 +375,7 @@ __host__ __device__ inline SmemLayout search_layout(int d, u32 width, u32 vis_sl
 #ifndef KNNG_SEARCH_MINB
 #define KNNG_SEARCH_MINB 1
 #endif
+template <bool kCos>
 __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const unsigned lane = lane_id();
@@ -392,6 +397,7 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
     // stage query, clear visited
     const float* qrow = a.Q + q * (u64)a.d;
     for (int t = lane; t < a.d; t += 32) s_q[t] = qrow[t];
+    const float qnorm = kCos ? a.qn[q] : 0.0f;
     for (u32 t = lane; t < a.vis_slots; t += 32) s_vis[t] = kNoId;
     __syncwarp();
     Visited vis{s_vis, a.vis_slots - 1, a.gtable ? a.gtable + (u64)blockIdx.x * a.gcap : nullptr,
@@ -409,7 +415,7 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
       }
     };
     auto score_and_merge = [&](u32 id, bool take) {
-      const u64 c = score_batch(a, s_q, s_stage, s_ptr, id, take);
+      const u64 c = score_batch<kCos>(a, s_q, s_stage, s_ptr, id, take, qnorm);
       beam_merge(c, s_beam, s_flag, s_clo, bs, W);
     };
 
@@ -573,7 +579,9 @@ void validate_search(uint64_t nq_dims, uint64_t v_dims, uint64_t sg_n, uint64_t 
 void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint32_t* sg,
                        uint32_t deg, const float* V, uint64_t nv, const SearchParamsDev& p,
                        uint32_t id_base, uint32_t* out_ids, float* out_d, uint32_t* hops,
-                       uint32_t* scored, SearchCounters* counters, uint64_t qbase) {
+                       uint32_t* scored, SearchCounters* counters, uint64_t qbase,
+                       const float* qn, const float* vn) {
+  require((qn == nullptr) == (vn == nullptr), "ann_search: cosine needs both norm arrays");
   validate_search((uint64_t)d, (uint64_t)d, nv, nv, p);
   if (nq == 0) return;
   DeviceGuard guard(r.device);
@@ -585,15 +593,19 @@ void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint
   // per-query diagnostics mirror the reference's exact visited-set size
   const bool exact = scored != nullptr || getenv("KNNG_SEARCH_EXACT") != nullptr;
   const SearchShape sh = search_shape(d, width, entries, exact);
-  KNNG_CUDA(cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  KNNG_CUDA(cudaFuncSetAttribute(k_search<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sh.smem));
+  KNNG_CUDA(cudaFuncSetAttribute(k_search<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sh.smem));
   int per_sm = 0;
-  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, 32, sh.smem));
+  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search<false>, 32, sh.smem));
   if (per_sm < 1) per_sm = 1;
   const unsigned grid = persistent_grid(r, per_sm, nq);
 
   SearchArgs a{};
   a.Q = Q;
+  a.qn = qn;
+  a.vn = vn;
   a.nq = nq;
   a.d = d;
   a.V = V;
@@ -631,7 +643,10 @@ void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint
   DBuf<u64> cnt(r, 4);
   cnt.zero();
   a.counters = cnt.p;
-  k_search<<<grid, 32, sh.smem, r.stream>>>(a);
+  if (qn)
+    k_search<true><<<grid, 32, sh.smem, r.stream>>>(a);
+  else
+    k_search<false><<<grid, 32, sh.smem, r.stream>>>(a);
   KNNG_LAUNCH_CHECK();
   if (counters) {
     u64 h[4];

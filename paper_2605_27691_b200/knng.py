@@ -297,6 +297,15 @@ def _is_u8(x) -> bool:
     return getattr(x, "dtype", None) == np.uint8
 
 
+def _metric_code(metric) -> int:
+    """metric_from_string core.cpp:13-16 ("l2" | "cosine"; MetricKind core.hpp:15)."""
+    if metric in (0, "l2"):
+        return 0
+    if metric in (1, "cosine"):
+        return 1
+    raise ValueError(f"unknown metric: {metric}")
+
+
 def _dataset(x, metric: int = 0) -> _Dataset:
     return _Dataset(_ptr(x), x.shape[0], x.shape[1], 1 if _is_u8(x) else 0, metric, _mem(x), 0)
 
@@ -500,13 +509,14 @@ def gen_random_dataset(n: int, dims: int, dist: str = "uniform", seed: int = 0,
     return out
 
 
-def row_distances(x, i: Sequence[int], j: Sequence[int], device: int = 0) -> np.ndarray:
+def row_distances(x, i: Sequence[int], j: Sequence[int], device: int = 0,
+                  metric: str = "l2") -> np.ndarray:
     """Dataset::row_distance core.hpp:84-95, batched, exact order."""
     x = _as_rows(x)
     i = np.ascontiguousarray(i, np.uint32)
     j = np.ascontiguousarray(j, np.uint32)
     out = np.empty(len(i), np.float32)
-    ds = _dataset(x)
+    ds = _dataset(x, _metric_code(metric))
     _check(lib().knng_row_distances(context().h, device, C.byref(ds), _ptr(i), _ptr(j), len(i),
                                     _ptr(out)))
     return out
@@ -536,7 +546,8 @@ def merge_rows(a_ids, a_d, b_ids, b_d, k: int):
     return oi[0, :oc[0]], od[0, :oc[0]]
 
 
-def init_random_graph(x, k: int, seed: int, device: Optional[int] = None) -> KnnGraph:
+def init_random_graph(x, k: int, seed: int, device: Optional[int] = None,
+                      metric: str = "l2") -> KnnGraph:
     """nndescent.cpp:29-62"""
     x = _as_rows(x)
     dev = _device_of(x) if device is None else device
@@ -544,7 +555,7 @@ def init_random_graph(x, k: int, seed: int, device: Optional[int] = None) -> Knn
     g = KnnGraph(_empty_like_mem(x, (n, k), np.uint32), _empty_like_mem(x, (n, k), np.float32),
                  _empty_like_mem(x, (n, k), np.uint8))
     cg = _Graph(_ptr(g.ids), _ptr(g.dists), _ptr(g.flags), n, k, _mem(x))
-    ds = _dataset(x)
+    ds = _dataset(x, _metric_code(metric))
     _check(lib().knng_init_random_graph(context().h, dev, C.byref(ds), k, seed, C.byref(cg)))
     return g
 
@@ -577,7 +588,7 @@ def sample_neighbors(graph: KnnGraph, rho: float, seed: int, iteration: int, dev
 
 
 def nn_descent(x, params: Optional[NnDescentParams] = None, stats: Optional[NnDescentStats] = None,
-               device: Optional[int] = None, **kw) -> KnnGraph:
+               device: Optional[int] = None, metric: str = "l2", **kw) -> KnnGraph:
     """nn_descent nndescent.cpp:225-259 (lock-free NN-Descent on the B200)."""
     p = params or NnDescentParams(**kw)
     x = _as_rows(x)
@@ -589,7 +600,7 @@ def nn_descent(x, params: Optional[NnDescentParams] = None, stats: Optional[NnDe
     g = KnnGraph(_empty_like_mem(x, (n, k), np.uint32), _empty_like_mem(x, (n, k), np.float32),
                  _empty_like_mem(x, (n, k), np.uint8))
     cg = _Graph(_ptr(g.ids), _ptr(g.dists), _ptr(g.flags), n, k, _mem(x))
-    ds = _dataset(x)
+    ds = _dataset(x, _metric_code(metric))
     cp = p._c()
     acc = np.zeros(max(p.max_iters, 1), np.uint64)
     st = _NndStats()
@@ -615,7 +626,7 @@ def nn_descent(x, params: Optional[NnDescentParams] = None, stats: Optional[NnDe
 
 
 def optimize_graph(graph: KnnGraph, x, out_degree: int = 0, workers: int = 0,
-                   device: Optional[int] = None):
+                   device: Optional[int] = None, metric: str = "l2"):
     """graphopt.cpp:24-105 -> n x out_degree search-graph ids."""
     x = _as_rows(x)
     dev = _device_of(x) if device is None else device
@@ -631,14 +642,15 @@ def optimize_graph(graph: KnnGraph, x, out_degree: int = 0, workers: int = 0,
         raise InvalidArgument("optimize_graph: out_degree must be <= k")
     sg = _empty_like_mem(graph.ids, (n, od), np.uint32)
     cg = _Graph(_ptr(ids), _ptr(dists), None, n, k, mem)
-    ds = _dataset(x)
+    ds = _dataset(x, _metric_code(metric))
     _check(lib().knng_optimize_graph(context().h, dev, C.byref(cg), C.byref(ds), out_degree,
                                      _ptr(sg)))
     return sg
 
 
 def ann_search(queries, sgraph, vectors, params: Optional[SearchParams] = None,
-               diagnostics: bool = False, device: Optional[int] = None, **kw) -> SearchResult:
+               diagnostics: bool = False, device: Optional[int] = None, metric: str = "l2",
+               **kw) -> SearchResult:
     """annsearch.cpp:50-129 (bit-identical to the reference's greedy search)."""
     p = params or SearchParams(**kw)
     q = _as_rows(queries)
@@ -656,7 +668,7 @@ def ann_search(queries, sgraph, vectors, params: Optional[SearchParams] = None,
     out_d = _empty_like_mem(q, (nq, p.k_s), np.float32)
     hops = _empty_like_mem(q, (nq,), np.uint32) if diagnostics else None
     scored = _empty_like_mem(q, (nq,), np.uint32) if diagnostics else None
-    qd, vd = _dataset(q), _dataset(v)
+    qd, vd = _dataset(q, _metric_code(metric)), _dataset(v, _metric_code(metric))
     if sg.size == 0 and mem == MEM_HOST:
         sg = np.zeros(1, np.uint32)
     _check(lib().knng_ann_search(context().h, dev, C.byref(qd), _ptr(sg), n_sg, deg, C.byref(vd),
@@ -725,7 +737,8 @@ class ThroughputRow:
 
 
 def search_throughput_probe(cases, queries, params: "SearchParams",
-                            device: Optional[int] = None) -> List[ThroughputRow]:
+                            device: Optional[int] = None,
+                            metric: str = "l2") -> List[ThroughputRow]:
     """annsearch.cpp:131-155: `cases` = [(source_count, sgraph, vectors), ...]
     in ascending source_count; seconds are device time of each search."""
     q = _as_rows(queries)
@@ -735,12 +748,12 @@ def search_throughput_probe(cases, queries, params: "SearchParams",
     for i, (count, sg, vec) in enumerate(cases):
         v = _as_rows(vec)
         sgm = sg if _is_torch_cuda(sg) else np.ascontiguousarray(sg, np.uint32)
-        ds = _dataset(v)
+        ds = _dataset(v, _metric_code(metric))
         keep += [v, sgm, ds]
         arr[i] = _ThroughputCase(count, _ptr(sgm), sgm.shape[0], sgm.shape[1], C.pointer(ds),
                                  _mem(sgm))
     rows = (_ThroughputRow * max(1, len(cases)))()
-    qd = _dataset(q)
+    qd = _dataset(q, _metric_code(metric))
     _check(lib().knng_search_throughput_probe(context().h, dev, arr, len(cases), C.byref(qd),
                                               C.byref(params._c()), rows))
     return [ThroughputRow(rows[i].source_count, rows[i].num_queries, rows[i].seconds,
@@ -825,7 +838,7 @@ def _dist_result(graph, r: _DistResult) -> DistBuildResult:
                            nnd_iterations=r.nnd_iterations)
 
 
-def build_distributed(x, cfg: RefineConfig) -> DistBuildResult:
+def build_distributed(x, cfg: RefineConfig, metric: str = "l2") -> DistBuildResult:
     """refine.cpp:504-586: partition -> local NN-Descent -> tree refine ->
     grouped merge -> flat refine -> external ids, on the context's GPUs
     (rank r on GPU r mod #GPUs)."""
@@ -834,7 +847,7 @@ def build_distributed(x, cfg: RefineConfig) -> DistBuildResult:
     k = cfg.k
     out = KnnGraph(_empty_like_mem(x, (n, k), np.uint32), _empty_like_mem(x, (n, k), np.float32))
     cg = _Graph(_ptr(out.ids), _ptr(out.dists), None, n, k, _mem(x))
-    ds = _dataset(x)
+    ds = _dataset(x, _metric_code(metric))
     res = _DistResult()
     cc = cfg._c()
     nsnap = 0
@@ -882,7 +895,8 @@ class RankBuildResult(DistBuildResult):
 
 
 def build_distributed_rank(x, cfg: RefineConfig, rank: int, world_size: int,
-                           allgather=None, device: Optional[int] = None) -> RankBuildResult:
+                           allgather=None, device: Optional[int] = None,
+                           metric: str = "l2") -> RankBuildResult:
     """One rank of build_distributed (refine.cpp:504-586) in this process, for
     one process per GPU.  Collective over `allgather(bytes_in, nbytes) ->
     bytes_out` (default: torch_allgather() on the default group).  Every rank
@@ -907,7 +921,7 @@ def build_distributed_rank(x, cfg: RefineConfig, rank: int, world_size: int,
             err.append(e)
             return 1
     cb = _ALLGATHER_FN(thunk)
-    ds = _dataset(x)
+    ds = _dataset(x, _metric_code(metric))
     res = _DistResult()
     cc = cfg._c()
     rows = _u64(0)
@@ -938,7 +952,7 @@ def refine(x_perm, cfg: RefineConfig, offsets, ids, dists, mode: int = 0) -> Dis
     return _dist_result(KnnGraph(ids, dists), res)
 
 
-def brute_force_knng(x, k: int, rows=None, device: Optional[int] = None):
+def brute_force_knng(x, k: int, rows=None, device: Optional[int] = None, metric: str = "l2"):
     """evalio.cpp:125-147 for `rows` (default all) -> (ids, dists) q x k."""
     x = _as_rows(x)
     dev = _device_of(x) if device is None else device
@@ -949,7 +963,7 @@ def brute_force_knng(x, k: int, rows=None, device: Optional[int] = None):
     q = len(rows)
     oi = _empty_like_mem(x, (q, k), np.uint32)
     od = _empty_like_mem(x, (q, k), np.float32)
-    ds = _dataset(x)
+    ds = _dataset(x, _metric_code(metric))
     _check(lib().knng_brute_force(context().h, dev, C.byref(ds), _ptr(rows), q, k, _mem(x),
                                   _ptr(oi), _ptr(od)))
     return oi, od
@@ -963,6 +977,26 @@ def recall_at_k(test_ids, truth_ids, k_eval: int) -> float:
     for r in range(t.shape[0]):
         hits += len(np.intersect1d(t[r], g[r], assume_unique=False))
     return hits / float(t.shape[0] * k_eval)
+
+
+def distance_threshold_recall(test_dists, ref_dists, k_eval: int) -> float:
+    """evalio.cpp:199-215 (host, measurement only): per row, the share of the
+    first k_eval test distances <= the reference row's k_eval-th distance,
+    averaged over rows in row order."""
+    t = np.asarray(test_dists, np.float32)
+    g = np.asarray(ref_dists, np.float32)
+    if k_eval == 0 or k_eval > t.shape[1] or k_eval > g.shape[1]:
+        raise InvalidArgument("distance_threshold_recall: k_eval out of range")
+    if t.shape[0] != g.shape[0]:
+        raise InvalidArgument("distance_threshold_recall: graphs not comparable")
+    thr = g[:, k_eval - 1:k_eval]
+    # rows are sorted, so the leading run <= thr is the count of entries <= thr
+    # only if the run is contiguous; count the run exactly as the reference does
+    run = np.cumprod(t <= thr, axis=1).sum(axis=1)
+    total = 0.0
+    for c in np.minimum(run, k_eval):
+        total += float(c) / float(k_eval)
+    return total / float(t.shape[0])
 
 
 def save_graph(graph: KnnGraph, path: str):

@@ -93,6 +93,26 @@ int main() {
     std::printf("  recall@10 = %.4f after %zu iterations\n", r, st.iterations);
     require(r >= 0.95, "recall@10 < 0.95");
   });
+  run("cosine datasets (MetricKind::cosine, core.hpp:41-55)", [] {
+    const Dataset d =
+        gen_random_dataset(5000, 24, Distribution::clustered, 7, 20, MetricKind::cosine);
+    NnDescentParams p;
+    p.k = 16;
+    p.seed = 1;
+    const KnnGraph g = nn_descent(d, p);
+    const GroundTruth gt = brute_force_knng(d, 16);
+    const double r = recall_at_k(g, gt, 10);
+    std::printf("  cosine recall@10 = %.4f\n", r);
+    require(r >= 0.9, "cosine recall@10 < 0.9");
+    RefineConfig cfg;
+    cfg.ranks = 2;
+    cfg.k = 16;
+    const DistBuildResult rd = build_distributed(d, cfg);
+    // the unmodified reference reaches 0.7702 on this data and config
+    const double r2 = recall_at_k(rd.graph, gt, 10);
+    std::printf("  cosine P=2 recall@10 = %.4f (reference 0.7702)\n", r2);
+    require(r2 >= 0.7702 - 0.02, "cosine P=2 recall below the reference's");
+  });
   run("P=1 build_distributed == nn_descent (test_refine.cpp:349-359)", [] {
     const Dataset d = gen_random_dataset(2000, 16, Distribution::clustered, 3, 10);
     RefineConfig cfg;

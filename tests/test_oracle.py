@@ -145,3 +145,43 @@ def test_tree_schedule_worked_example(oracle):
     assert L.ko_tree_schedule(8, 2, 0, 1, C.byref(hi), partners) == 0
     assert list(partners[:2]) == [2, 3] and hi.value == 2
     assert L.ko_tree_levels(8, 2) == 2 and L.ko_tree_levels(4, 4) == 0
+
+
+# ---------------------------------------------------------------------------
+# cosine metric (core.hpp:41-55), pinned by tests/golden/cosine.npz (minted
+# from the reference with MetricKind::cosine datasets)
+# ---------------------------------------------------------------------------
+
+
+def test_cosine_golden_values(oracle):
+    # test_core.cpp:55-70: parallel -> 0, orthogonal -> 1, zero vector -> 1
+    assert oracle.cosine([1.0, 2.0], [2.0, 4.0]) == 0.0
+    assert oracle.cosine([1.0, 0.0], [0.0, 3.0]) == 1.0
+    assert oracle.cosine([0.0, 0.0], [1.0, 1.0]) == 1.0
+
+
+def test_cosine_pairs(golden, oracle):
+    g = golden("cosine")
+    x = g["x"]
+    d = np.array([oracle.cosine(x[a], x[b]) for a, b in zip(g["pair_i"], g["pair_j"])],
+                 np.float32)
+    assert np.array_equal(bits(d), bits(g["pair_d"]))
+    x7 = g["x7"]
+    d7 = np.array([oracle.cosine(x7[a], x7[299 - a]) for a in range(300)], np.float32)
+    assert np.array_equal(bits(d7), bits(g["pair7_d"]))
+
+
+def test_cosine_stages(golden, oracle):
+    g = golden("cosine")
+    x = g["x"]
+    ii, idd, _ = oracle.init_random_graph(x, 12, 5, metric=1)
+    assert np.array_equal(ii, g["init_ids"]) and np.array_equal(bits(idd), bits(g["init_d"]))
+    ni, nd, _, _ = oracle.nn_descent(x, 16, seed=3, metric=1)
+    assert np.array_equal(ni, g["nn_ids"]) and np.array_equal(bits(nd), bits(g["nn_d"]))
+    assert np.array_equal(oracle.optimize_graph(g["nn_ids"], g["nn_d"], x, 16, metric=1), g["sg"])
+    assert np.array_equal(oracle.optimize_graph(g["nn_ids"], g["nn_d"], x, 8, metric=1), g["sg8"])
+    i, d, h, s = oracle.ann_search(g["q"], g["sg"], x, 16, 64, 16, 0, 9, metric=1)
+    assert np.array_equal(i, g["s_ids"]) and np.array_equal(bits(d), bits(g["s_d"]))
+    assert np.array_equal(h, g["s_hops"]) and np.array_equal(s, g["s_scored"])
+    bi, bd = oracle.brute_force_rows(x, np.arange(len(x)), 10, metric=1)
+    assert np.array_equal(bi, g["bf_ids"]) and np.array_equal(bits(bd), bits(g["bf_d"]))
