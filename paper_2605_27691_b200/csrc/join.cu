@@ -17,6 +17,7 @@
 //   k_offer       resolves queued offers into the 4-way candidate buckets with
 //                 atomicMin cascades (lock-free, order-independent).
 #include <algorithm>
+#include <cstdlib>
 
 #include "join.hpp"
 #include "nndescent.hpp"
@@ -330,12 +331,14 @@ __device__ bool load_chunk(const JoinArgs& a, const Smem& s, int m) {
     s.cnt(m)[tid] = a.L_cnt[pt];
   }
   __syncthreads();
-  for (int e = tid; e < np * a.RMAX; e += kJT) {
-    const int j = e / a.RMAX, i = e - j * a.RMAX;
-    if (i < (int)(s.cnt(m)[j] >> 16)) {
-      const u32 id = a.L_ids[(u64)s.pid(m)[j] * a.RMAX + i];
-      s.ids(m)[e] = id;
-      s.worst(m)[e] = a.worst[id];
+  // warp per point, lane per list entry (no index division; empty slots skipped)
+  for (int j = tid >> 5; j < np; j += kJT / 32) {
+    const int na = (int)(s.cnt(m)[j] >> 16);
+    const u32* src = a.L_ids + (u64)s.pid(m)[j] * a.RMAX;
+    for (int i = tid & 31; i < na; i += 32) {
+      const u32 id = src[i];
+      s.ids(m)[j * a.RMAX + i] = id;
+      s.worst(m)[j * a.RMAX + i] = a.worst[id];
     }
   }
   if (tid == 0) {
@@ -423,10 +426,14 @@ __device__ void issue_rows(const JoinArgs& a, const Smem& s, int q, int c0, int 
   const u32* rowid = s.rowid(q);
   float* xb = s.x(buf);
   if ((a.d & 3) == 0) {
-    const int qd = dc >> 2;
-    for (int e = threadIdx.x; e < rows * qd; e += kJT) {
-      const int r = e / qd, c4 = e - r * qd;
-      cp_async16(xb + r * a.DCP + c4 * 4, a.X + (u64)rowid[r] * a.d + c0 + c4 * 4);
+    // thread -> (row r0 + k * rpi, 16-byte piece c4): one division per call
+    const int qd = dc >> 2, rpi = kJT / qd;
+    const int r0 = (int)threadIdx.x / qd, c4 = (int)threadIdx.x - r0 * qd;
+    if (r0 < rpi) {
+      const float* src = a.X + c0 + c4 * 4;
+      float* dst = xb + c4 * 4;
+      for (int r = r0; r < rows; r += rpi)
+        cp_async16(dst + r * a.DCP, src + (u64)rowid[r] * (u64)a.d);
     }
   } else {
     for (int e = threadIdx.x; e < rows * dc; e += kJT) {
@@ -715,10 +722,12 @@ JoinPlan plan_join(const Runner& r, int d, uint32_t k, uint32_t B) {
   JoinPlan p;
   const int max_rows = (int)(2 * B + k + B);
   p.RMAX = (max_rows + 3) & ~3;
-  // Stage 32 dims at a time: a batch then holds ~430 rows = ~512 tiles, i.e.
-  // exactly 2 tiles per thread; the exact-order accumulators carry across
-  // the dim slices (registers), so the summation order is unchanged.
-  p.DC = d <= 32 ? ((d + 7) & ~7) : 32;
+  // Stage DC dims at a time (default 32); the exact-order accumulators carry
+  // across the dim slices (registers), so the summation order is unchanged.
+  // A narrower slice fits more rows (points) per batch: KNNG_JOIN_DC tunes it.
+  int dc = 32;
+  if (const char* v = std::getenv("KNNG_JOIN_DC")) dc = std::max(8, (std::atoi(v) + 7) & ~7);
+  p.DC = d <= dc ? ((d + 7) & ~7) : dc;
   p.DCP = p.DC + 4;  // DC % 8 == 0 -> (DCP/4) odd: conflict-free LDS.128 across rows
   int smem_max = 0;
   KNNG_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, r.device));
