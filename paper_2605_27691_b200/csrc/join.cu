@@ -252,7 +252,10 @@ struct Tile {
   bool tri;
 };
 
-// per meta slot (2): s_ids[G*RMAX] u32 | s_worst[G*RMAX] f32 | s_cnt[G] | s_pid[G] | hdr[4]
+// per meta slot (2): s_ids[G*RMAX] u32 | s_cnt[G] | s_pid[G] | hdr[4]
+// (the worst snapshot is read from HBM/L2 per tile row and column: 4 MB at
+// 1M points stays L2-resident, and the smem it would take buys ~70 more
+// staged rows per batch, i.e. more tiles per CTA barrier)
 // per desc slot (2): s_rb[G+1] | s_tb[G+1] | hdr[4]
 // misc[16] | x[2][(RB+4)*DCP]
 // Slots are addressed arithmetically (base + slot * stride) so nothing lands
@@ -265,17 +268,14 @@ struct Smem {
   int RMAX;
   u32 meta_bytes, desc_bytes, xstride;
   __device__ u32* ids(int m) const { return reinterpret_cast<u32*>(meta + m * meta_bytes); }
-  __device__ float* worst(int m) const {
-    return reinterpret_cast<float*>(meta + m * meta_bytes + G * RMAX * 4);
-  }
   __device__ u32* cnt(int m) const {
-    return reinterpret_cast<u32*>(meta + m * meta_bytes + G * RMAX * 8);
+    return reinterpret_cast<u32*>(meta + m * meta_bytes + G * RMAX * 4);
   }
   __device__ u32* pid(int m) const {
-    return reinterpret_cast<u32*>(meta + m * meta_bytes + G * RMAX * 8 + G * 4);
+    return reinterpret_cast<u32*>(meta + m * meta_bytes + G * RMAX * 4 + G * 4);
   }
   __device__ int* mhdr(int m) const {  // [0] chunk, [1] np, [2] offers queued
-    return reinterpret_cast<int*>(meta + m * meta_bytes + G * RMAX * 8 + G * 8);
+    return reinterpret_cast<int*>(meta + m * meta_bytes + G * RMAX * 4 + G * 8);
   }
   __device__ int* rb(int q) const { return reinterpret_cast<int*>(desc + q * desc_bytes); }
   __device__ int* tb(int q) const { return rb(q) + (G + 1); }
@@ -292,7 +292,7 @@ __host__ __device__ inline size_t desc_slot_bytes(int RB) {
 __device__ __forceinline__ Smem carve(unsigned char* base, int RMAX, int RB, int DCP) {
   Smem s;
   s.RMAX = RMAX;
-  s.meta_bytes = (u32)((size_t)G * RMAX * 8 + G * 8 + 16);
+  s.meta_bytes = (u32)((size_t)G * RMAX * 4 + G * 8 + 16);
   s.desc_bytes = (u32)desc_slot_bytes(RB);
   s.meta = base;
   s.desc = base + 2 * s.meta_bytes;
@@ -305,7 +305,7 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int RMAX, int RB, int
 }
 
 __host__ __device__ inline size_t join_smem_bytes(int RMAX, int RB, int DCP) {
-  size_t off = 2 * ((size_t)G * RMAX * 8 + G * 8 + 16) + 2 * desc_slot_bytes(RB) + 128;
+  size_t off = 2 * ((size_t)G * RMAX * 4 + G * 8 + 16) + 2 * desc_slot_bytes(RB) + 128;
   off = (off + 15) & ~size_t(15);
   return off + 2 * (size_t)(RB + 4) * DCP * 4;
 }
@@ -335,11 +335,7 @@ __device__ bool load_chunk(const JoinArgs& a, const Smem& s, int m) {
   for (int j = tid >> 5; j < np; j += kJT / 32) {
     const int na = (int)(s.cnt(m)[j] >> 16);
     const u32* src = a.L_ids + (u64)s.pid(m)[j] * a.RMAX;
-    for (int i = tid & 31; i < na; i += 32) {
-      const u32 id = src[i];
-      s.ids(m)[j * a.RMAX + i] = id;
-      s.worst(m)[j * a.RMAX + i] = a.worst[id];
-    }
+    for (int i = tid & 31; i < na; i += 32) s.ids(m)[j * a.RMAX + i] = src[i];
   }
   if (tid == 0) {
     s.mhdr(m)[0] = (int)chunk;
@@ -592,31 +588,37 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
         pass_mask[t] = 0;
         if (T[t].pt < 0) continue;
         const int lb = T[t].pt * a.RMAX;
+        // ids and worst snapshots of the tile's 4 rows and 4 columns
+        u32 rid[4], cid[4];
+        float rw[4], cw[4];
+        const int cbase = T[t].tri ? 0 : T[t].nn;
+        const int clim = T[t].tri ? T[t].nn : T[t].no;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int i = T[t].ti + T[t].rstr * q4, jj = T[t].tj + T[t].cstr * q4;
+          rid[q4] = i < T[t].nn ? s.ids(m)[lb + i] : 0u;
+          cid[q4] = jj < clim ? s.ids(m)[lb + cbase + jj] : 0u;
+          rw[q4] = i < T[t].nn ? __ldg(a.worst + rid[q4]) : 0.0f;
+          cw[q4] = jj < clim ? __ldg(a.worst + cid[q4]) : 0.0f;
+        }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int i = T[t].ti + T[t].rstr * r;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const int jj = T[t].tj + T[t].cstr * c;
-            bool valid;
-            int jl;
-            if (T[t].tri) {
-              valid = i < T[t].nn && jj < T[t].nn && (T[t].ti < T[t].tj || r < c);
-              jl = jj;
-            } else {
-              valid = i < T[t].nn && jj < T[t].no;
-              jl = T[t].nn + jj;
-            }
+            const bool valid =
+                T[t].tri ? (i < T[t].nn && jj < T[t].nn && (T[t].ti < T[t].tj || r < c))
+                         : (i < T[t].nn && jj < T[t].no);
             if (!valid) continue;
             const float dist =
-                kCos ? cos_finish(acc[t][r][c], __ldg(a.nrm + s.ids(m)[lb + i]),
-                                  __ldg(a.nrm + s.ids(m)[lb + jl]))
+                kCos ? cos_finish(acc[t][r][c], __ldg(a.nrm + rid[r]), __ldg(a.nrm + cid[c]))
                      : __fsqrt_rn(acc[t][r][c]);
             acc[t][r][c] = dist;
             ++my_pairs;
             const int bit = (r * 4 + c) * 2;
-            if (dist < s.worst(m)[lb + i]) pass_mask[t] |= 1u << bit;
-            if (dist < s.worst(m)[lb + jl]) pass_mask[t] |= 2u << bit;
+            if (dist < rw[r]) pass_mask[t] |= 1u << bit;
+            if (dist < cw[c]) pass_mask[t] |= 2u << bit;
           }
         }
         my_q += __popc(pass_mask[t]);
