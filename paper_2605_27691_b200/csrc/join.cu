@@ -588,9 +588,9 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
         pass_mask[t] = 0;
         if (T[t].pt < 0) continue;
         const int lb = T[t].pt * a.RMAX;
-        // ids and worst snapshots of the tile's 4 rows and 4 columns
+        // ids, worst snapshots (and cosine norm chains) of the tile's 4 rows and 4 columns
         u32 rid[4], cid[4];
-        float rw[4], cw[4];
+        float rw[4], cw[4], rn[4], cn[4];
         const int cbase = T[t].tri ? 0 : T[t].nn;
         const int clim = T[t].tri ? T[t].nn : T[t].no;
 #pragma unroll
@@ -600,6 +600,8 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
           cid[q4] = jj < clim ? s.ids(m)[lb + cbase + jj] : 0u;
           rw[q4] = i < T[t].nn ? __ldg(a.worst + rid[q4]) : 0.0f;
           cw[q4] = jj < clim ? __ldg(a.worst + cid[q4]) : 0.0f;
+          rn[q4] = kCos ? __ldg(a.nrm + rid[q4]) : 0.0f;
+          cn[q4] = kCos ? __ldg(a.nrm + cid[q4]) : 0.0f;
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -611,9 +613,7 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
                 T[t].tri ? (i < T[t].nn && jj < T[t].nn && (T[t].ti < T[t].tj || r < c))
                          : (i < T[t].nn && jj < T[t].no);
             if (!valid) continue;
-            const float dist =
-                kCos ? cos_finish(acc[t][r][c], __ldg(a.nrm + rid[r]), __ldg(a.nrm + cid[c]))
-                     : __fsqrt_rn(acc[t][r][c]);
+            const float dist = m_finish<kCos>(acc[t][r][c], rn[r], cn[c]);
             acc[t][r][c] = dist;
             ++my_pairs;
             const int bit = (r * 4 + c) * 2;
