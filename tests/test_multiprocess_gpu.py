@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, port, n, d, out_dir):
+def _rank_main(rank, world, port, n, d, out_dir, metric="l2"):
     import torch
     import torch.distributed as dist
     import paper_2605_27691_b200 as knng
@@ -32,12 +32,12 @@ def _rank_main(rank, world, port, n, d, out_dir):
                             nn=knng.NnDescentParams(k=16, seed=3),
                             search=knng.SearchParams(k_s=16, beam_width=64, num_entry_points=32,
                                                      seed=5))
-    r = knng.build_distributed_rank(x, cfg, rank, world)
+    r = knng.build_distributed_rank(x, cfg, rank, world, metric=metric)
     # the same rank from pinned host memory (each rank gathers only its block
     # over PCIe) must give the identical rows
     xh = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
     xh.copy_(x.cpu())
-    rh = knng.build_distributed_rank(xh.numpy(), cfg, rank, world, device=dev)
+    rh = knng.build_distributed_rank(xh.numpy(), cfg, rank, world, device=dev, metric=metric)
     assert np.array_equal(rh.graph.ids, r.graph.ids.cpu().numpy())
     assert np.array_equal(rh.rows, r.rows.cpu().numpy())
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=r.graph.ids.cpu().numpy(),
@@ -47,18 +47,18 @@ def _rank_main(rank, world, port, n, d, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_rank_processes_match_single_process(knng, tmp_path, world):
+@pytest.mark.parametrize("world,metric", [(2, "l2"), (4, "l2"), (8, "l2"), (4, "cosine")])
+def test_rank_processes_match_single_process(knng, tmp_path, world, metric):
     import torch.multiprocessing as mp
     n, d = 12_000, 24
-    mp.start_processes(_rank_main, args=(world, _free_port(), n, d, str(tmp_path)),
+    mp.start_processes(_rank_main, args=(world, _free_port(), n, d, str(tmp_path), metric),
                        nprocs=world, join=True, start_method="spawn")
     x = knng.gen_random_dataset(n, d, "clustered", 42, 16)
     cfg = knng.RefineConfig(ranks=world, groups=2, k=16, seed=7,
                             nn=knng.NnDescentParams(k=16, seed=3),
                             search=knng.SearchParams(k_s=16, beam_width=64, num_entry_points=32,
                                                      seed=5))
-    ref = knng.build_distributed(x, cfg)
+    ref = knng.build_distributed(x, cfg, metric=metric)
     seen = np.zeros(n, bool)
     for rank in range(world):
         z = np.load(tmp_path / f"rank{rank}.npz")
