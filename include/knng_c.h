@@ -278,7 +278,9 @@ knng_status knng_build_distributed_rank(knng_ctx* ctx, int device, uint64_t rank
 /* World-level drivers from given local graphs (internal global ids):
  * mode 0 = binary_tree_refine -> grouped_merge -> flat_refine,
  * mode 1 = all_to_all_refine (refine.hpp:117-136).  x_perm: rows in internal
- * order (host); ids/dists updated in place (host). */
+ * order (host, f32, l2 metric: the raw-row signature carries no metric --
+ * cosine datasets go through knng_build_distributed[_rank]); ids/dists
+ * updated in place (host). */
 knng_status knng_refine(knng_ctx* ctx, const float* x_perm, uint64_t n, uint64_t dims,
                         const knng_refine_config* cfg, const uint64_t* offsets, uint32_t* ids,
                         float* dists, int mode, knng_dist_result* result);
