@@ -122,7 +122,10 @@ __global__ __launch_bounds__(256) void k_join_lists(u64 n, u32 k, u32 B, int RMA
 // ---------------------------------------------------------------------------
 // k_offer
 // ---------------------------------------------------------------------------
-constexpr int kOfferBatch = 2;  // offers per thread (rounds keep their atomics independent)
+#ifndef KNNG_OFFER_BATCH
+#define KNNG_OFFER_BATCH 2
+#endif
+constexpr int kOfferBatch = KNNG_OFFER_BATCH;  // offers per thread (independent atomics per round)
 
 __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
                                                const u32* __restrict__ q_tgt,
@@ -486,7 +489,7 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Smem s = carve(smem, a.RMAX, a.RB, a.DCP);
   const int tid = threadIdx.x;
-  const unsigned lane = lane_id(), warp = tid >> 5;
+  const unsigned lane = lane_id();
   u64 my_pairs = 0, my_rows = 0, my_offers = 0;
   int pend_chunk = -1, pend_m = 0;  // chunk completed by the last batch (uniform)
 
