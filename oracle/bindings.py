@@ -327,6 +327,9 @@ class Ref:
                                             C.POINTER(CRefineCfg), u32p, f32p]
         L.kr_refine_from_local.argtypes = [f32p, C.c_uint64, C.c_uint64, C.POINTER(CRefineCfg),
                                            u32p, f32p, C.c_int, C.c_void_p]
+        L.kr_build_distributed_staged.argtypes = [f32p, C.c_uint64, C.c_uint64,
+                                                  C.POINTER(CRefineCfg), u32p, f32p, f64p,
+                                                  C.c_double]
 
     def _chk(self, rc):
         if rc == 1:
@@ -456,6 +459,18 @@ class Ref:
         self._chk(self.L.kr_build_distributed(x, n, dm, C.byref(cfg), ids, d, ph,
                                               C.byref(gets), C.byref(by)))
         return ids, d, ph, gets.value, by.value
+
+    def build_distributed_staged(self, x, cfg, watchdog_s=6 * 3600.0):
+        """build_distributed with concurrent local builds and a long barrier
+        watchdog (ref_capi.cpp kr_build_distributed_staged): the large-N
+        reference runs.  Returns external-id graph + (local, tree, merge, flat) s."""
+        n, dm = x.shape
+        ids = np.empty((n, cfg.k), np.uint32)
+        d = np.empty((n, cfg.k), np.float32)
+        ph = np.zeros(4, np.float64)
+        self._chk(self.L.kr_build_distributed_staged(x, n, dm, C.byref(cfg), ids, d, ph,
+                                                     watchdog_s))
+        return ids, d, ph
 
     def build_local_graphs(self, x, cfg):
         n, dm = x.shape

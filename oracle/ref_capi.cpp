@@ -372,4 +372,86 @@ int kr_refine_from_local(const float* data, std::uint64_t n, std::uint64_t dims,
   });
 }
 
+
+// build_distributed (refine.cpp:504-586) at sizes where the reference's own
+// driver cannot finish on this host: the P local builds run as P concurrent
+// threads exactly as local_build_rank (refine.cpp:380-390: workers=1, seed
+// mix_seed(nn.seed, rank) when P>1, ids shifted by offsets[rank]) -- the
+// reference's build_local_graphs runs them one after another -- and the
+// refine phases run through the public world drivers (refine.hpp:119-130)
+// with a barrier watchdog of `watchdog_s` seconds instead of 60 s (ranks'
+// multi-minute single-threaded phases finish more than a minute apart).
+// Output: the N x k graph in external ids, rows sorted by (dist, ext id) as
+// translate_to_external (refine.cpp:395-416).  phases = local, tree, merge, flat s.
+int kr_build_distributed_staged(const float* data, std::uint64_t n, std::uint64_t dims,
+                                const CRefineCfg* c, std::uint32_t* ids, float* dists,
+                                double* phases, double watchdog_s) {
+  return guard([&] {
+    const Dataset d = make_ds(data, n, dims);
+    const RefineConfig cfg = to_cfg(c);
+    const Partition part = partition_dataset(d, cfg.ranks, cfg.seed);
+    const std::size_t P = cfg.ranks;
+    using clk = std::chrono::steady_clock;
+    auto secs = [](clk::time_point a, clk::time_point b) {
+      return std::chrono::duration<double>(b - a).count();
+    };
+    auto t0 = clk::now();
+    std::vector<KnnGraph> gs(P);
+    std::vector<std::exception_ptr> errs(P);
+    {
+      std::vector<std::thread> th;
+      for (std::size_t r = 0; r < P; ++r)
+        th.emplace_back([&, r] {
+          try {
+            NnDescentParams np = cfg.nn;
+            np.k = cfg.k;
+            np.workers = 1;
+            np.seed = P == 1 ? cfg.nn.seed : mix_seed(cfg.nn.seed, r);
+            KnnGraph g = nn_descent(part.locals[r], np);
+            for (auto& id : g.ids) id += static_cast<std::uint32_t>(part.offsets[r]);
+            g.id_space = IdSpace::global;
+            gs[r] = std::move(g);
+          } catch (...) {
+            errs[r] = std::current_exception();
+          }
+        });
+      for (auto& t : th) t.join();
+      for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    }
+    auto t1 = clk::now();
+    const auto wd = std::chrono::milliseconds(static_cast<long long>(watchdog_s * 1000));
+    RankWorld w1(P, wd);
+    auto g1 = binary_tree_refine(w1, part, gs, cfg);
+    auto t2 = clk::now();
+    RankWorld w2(P, wd);
+    auto sgs = grouped_merge(w2, part, g1, cfg);
+    auto t3 = clk::now();
+    RankWorld w3(P, wd);
+    auto out = flat_refine(w3, part, g1, sgs, cfg);
+    auto t4 = clk::now();
+    const std::size_t k = cfg.k;
+    for (std::size_t r = 0; r < P; ++r) {
+      const KnnGraph& g = out[r];
+      for (std::size_t row = 0; row < g.num_sources; ++row) {
+        auto e = g.row_entries(row);
+        for (auto& x : e) x.id = part.to_external[x.id];
+        std::sort(e.begin(), e.end(),
+                  [](const NeighborEntry& a, const NeighborEntry& b) { return closer(a, b); });
+        const std::size_t ext = part.to_external[part.offsets[r] + row];
+        for (std::size_t j = 0; j < k; ++j) {
+          ids[ext * k + j] = e[j].id;
+          dists[ext * k + j] = e[j].dist;
+        }
+      }
+    }
+    if (phases) {
+      phases[0] = secs(t0, t1);
+      phases[1] = secs(t1, t2);
+      phases[2] = secs(t2, t3);
+      phases[3] = secs(t3, t4);
+    }
+  });
+}
+
 }  // extern "C"

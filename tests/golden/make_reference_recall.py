@@ -41,6 +41,12 @@ CONFIGS = {
     "dist_p2_2m_clustered16_k32": (2_000_000, 128, "clustered", 16, 32, 2, 128, 96),
     "dist_p4_4m_clustered16_k32": (4_000_000, 128, "clustered", 16, 32, 4, 128, 96),
     "dist_p8_8m_clustered16_k32": (8_000_000, 128, "clustered", 16, 32, 8, 128, 96),
+    # C4 (BASELINE configs[3]): 10M x 96 clustered(16), P=2/4/8, M=2 -- the reference's
+    # P single-threaded local builds run concurrently and its barrier watchdog is
+    # lengthened (kr_build_distributed_staged); otherwise build_distributed unchanged
+    "c4_10m_d96_clustered16_p2": (10_000_000, 96, "clustered", 16, 32, 2, 128, 96),
+    "c4_10m_d96_clustered16_p4": (10_000_000, 96, "clustered", 16, 32, 4, 128, 96),
+    "c4_10m_d96_clustered16_p8": (10_000_000, 96, "clustered", 16, 32, 8, 128, 96),
 }
 
 
@@ -77,6 +83,12 @@ def main():
         elif ranks == 1:
             ids, _, _, acc, secs = R.nn_descent(x, k, seed=1, workers=0)
             iters = len(acc)
+        elif name.startswith("c4_"):
+            cfg = R.refine_config(ranks, 2, k, nn_seed=1, search_seed=1, seed=1,
+                                  beam_width=beam, num_entry_points=entries)
+            ids, _, ph = R.build_distributed_staged(x, cfg)
+            secs, iters = time.time() - t, None
+            print(name, "phases local/tree/merge/flat s:", list(ph), flush=True)
         else:
             cfg = R.refine_config(ranks, 2, k, nn_seed=1, search_seed=1, seed=1,
                                   beam_width=beam, num_entry_points=entries)

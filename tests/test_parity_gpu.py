@@ -430,7 +430,10 @@ def _sample(n):
 
 @pytest.mark.parametrize("name", ["c1_100k_uniform_k10", "c1b_100k_clustered100_k32",
                                   "c4r_100k_d96_clustered16_p1", "c4r_100k_d96_clustered16_p2",
-                                  "c4r_100k_d96_clustered16_p4", "c4r_100k_d96_clustered16_p8"])
+                                  "c4r_100k_d96_clustered16_p4", "c4r_100k_d96_clustered16_p8",
+                                  # BASELINE configs[1..3] at full size
+                                  "c2_1m_clustered1000_k32", "c3_1m_d960_clustered1000_k32",
+                                  "c4_10m_d96_clustered16_p2", "c4_10m_d96_clustered16_p4"])
 def test_recall_parity_vs_reference(knng, name):
     ref = _ref_recall().get(name)
     if ref is None:
