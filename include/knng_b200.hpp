@@ -7,9 +7,15 @@
 // (partition -> local build -> remote refine -> merge -> graph output).
 // Internal building blocks of the CPU implementation that the GPU design does
 // not have (CandidateBuffer, NeighborSamples' vectors, local_join,
-// parallel_for, RankWorld) are not part of this surface; see INTEGRATION.md.
+// parallel_for) are not part of this surface; see INTEGRATION.md.  The
+// host-side parts of the reference API (Rng, wire regions, RankWorld and its
+// world-level phase drivers, the cost model) are in knng_b200_host.hpp,
+// included at the end; include/knng/*.hpp forward the reference's header
+// names here, so the reference's own sources compile unchanged against it.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <filesystem>
 #include <memory>
@@ -63,7 +69,62 @@ inline knng_ctx* ctx() {
 }
 }  // namespace detail
 
-// Dataset core.hpp:67-105 (f32 / l2 on the B200 path)
+inline const char* to_string(MetricKind m) { return m == MetricKind::l2 ? "l2" : "cosine"; }
+inline MetricKind metric_from_string(const std::string& s) {
+  if (s == "l2") return MetricKind::l2;
+  if (s == "cosine") return MetricKind::cosine;
+  throw std::invalid_argument("unknown metric: " + s);
+}
+
+// sigma core.hpp:23-55 on the host (the exact operation order of the
+// reference: per dimension a separately rounded subtract, multiply and add,
+// then sqrt -- compile callers with -ffp-contract=off).  The library computes
+// every distance of a build on the GPU in this same order; these host forms
+// serve measurement code and Dataset::row_distance.
+namespace detail {
+template <class T>
+inline float l2_exact(const T* a, const T* b, std::size_t d) {
+  float acc = 0.0f;
+  for (std::size_t i = 0; i < d; ++i) {
+    const float t = static_cast<float>(a[i]) - static_cast<float>(b[i]);
+    const float sq = t * t;
+    acc = acc + sq;
+  }
+  return std::sqrt(acc);
+}
+inline float l2_f32(const float* a, const float* b, std::size_t d) { return l2_exact(a, b, d); }
+inline float l2_u8(const std::uint8_t* a, const std::uint8_t* b, std::size_t d) {
+  return l2_exact(a, b, d);
+}
+template <class T>
+inline float cosine_t(const T* a, const T* b, std::size_t d) {
+  float dot = 0.0f, na = 0.0f, nb = 0.0f;
+  for (std::size_t i = 0; i < d; ++i) {
+    const float x = static_cast<float>(a[i]), y = static_cast<float>(b[i]);
+    const float xy = x * y, xx = x * x, yy = y * y;
+    dot = dot + xy;
+    na = na + xx;
+    nb = nb + yy;
+  }
+  if (na == 0.0f || nb == 0.0f) return 1.0f;
+  const float v = 1.0f - dot / (std::sqrt(na) * std::sqrt(nb));
+  return v < 0.0f ? 0.0f : v;
+}
+}  // namespace detail
+
+inline float distance(MetricKind m, std::span<const float> a, std::span<const float> b) {
+  if (a.size() != b.size()) throw std::invalid_argument("distance: dimension mismatch");
+  return m == MetricKind::l2 ? detail::l2_f32(a.data(), b.data(), a.size())
+                             : detail::cosine_t(a.data(), b.data(), a.size());
+}
+inline float distance(MetricKind m, std::span<const std::uint8_t> a,
+                      std::span<const std::uint8_t> b) {
+  if (a.size() != b.size()) throw std::invalid_argument("distance: dimension mismatch");
+  return m == MetricKind::l2 ? detail::l2_u8(a.data(), b.data(), a.size())
+                             : detail::cosine_t(a.data(), b.data(), a.size());
+}
+
+// Dataset core.hpp:67-105 (f32 or u8 rows; l2 or cosine)
 struct Dataset {
   std::size_t num_points = 0;
   std::size_t dims = 0;
@@ -80,11 +141,79 @@ struct Dataset {
     return d;
   }
   std::span<const float> frow(std::size_t i) const { return {f32.data() + i * dims, dims}; }
+  std::span<const std::uint8_t> brow(std::size_t i) const {
+    return {u8.data() + i * dims, dims};
+  }
+  float row_distance(std::size_t i, std::size_t j) const {
+    if (elem_kind == ElemKind::f32)
+      return metric == MetricKind::l2
+                 ? detail::l2_f32(f32.data() + i * dims, f32.data() + j * dims, dims)
+                 : detail::cosine_t(f32.data() + i * dims, f32.data() + j * dims, dims);
+    return metric == MetricKind::l2
+               ? detail::l2_u8(u8.data() + i * dims, u8.data() + j * dims, dims)
+               : detail::cosine_t(u8.data() + i * dims, u8.data() + j * dims, dims);
+  }
+  Dataset slice(std::size_t begin, std::size_t count) const {
+    if (begin + count > num_points) throw std::invalid_argument("Dataset::slice out of range");
+    Dataset out = empty(dims, elem_kind, metric);
+    out.num_points = count;
+    if (elem_kind == ElemKind::f32)
+      out.f32.assign(f32.begin() + begin * dims, f32.begin() + (begin + count) * dims);
+    else
+      out.u8.assign(u8.begin() + begin * dims, u8.begin() + (begin + count) * dims);
+    return out;
+  }
+  void append(const Dataset& o) {
+    if (o.dims != dims || o.elem_kind != elem_kind || o.metric != metric)
+      throw std::invalid_argument("Dataset::append: incompatible dataset");
+    if (elem_kind == ElemKind::f32)
+      f32.insert(f32.end(), o.f32.begin(), o.f32.end());
+    else
+      u8.insert(u8.end(), o.u8.begin(), o.u8.end());
+    num_points += o.num_points;
+  }
+  // FNV-1a over (num_points, dims), (elem kind, metric) and the payload bytes
+  std::uint64_t content_hash() const {
+    std::uint64_t h = 0xcbf29ce484222325ULL;
+    auto mix = [&h](const void* p, std::size_t n) {
+      const unsigned char* c = static_cast<const unsigned char*>(p);
+      for (std::size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 0x100000001b3ULL;
+    };
+    const std::uint64_t shape[2] = {num_points, dims};
+    const std::uint8_t tag[2] = {static_cast<std::uint8_t>(elem_kind),
+                                 static_cast<std::uint8_t>(metric)};
+    mix(shape, sizeof shape);
+    mix(tag, sizeof tag);
+    if (elem_kind == ElemKind::f32)
+      mix(f32.data(), f32.size() * sizeof(float));
+    else
+      mix(u8.data(), u8.size());
+    return h;
+  }
+  std::size_t payload_bytes() const {
+    return elem_kind == ElemKind::f32 ? f32.size() * sizeof(float) : u8.size();
+  }
+  void validate() const {
+    if ((elem_kind == ElemKind::f32 ? f32.size() : u8.size()) != num_points * dims)
+      throw std::logic_error("Dataset: data length != num_points * dims");
+  }
   knng_dataset view() const {
-    return knng_dataset{f32.data(), num_points, dims, static_cast<std::uint8_t>(elem_kind),
+    const void* data = elem_kind == ElemKind::u8 ? static_cast<const void*>(u8.data())
+                                                 : static_cast<const void*>(f32.data());
+    return knng_dataset{data, num_points, dims, static_cast<std::uint8_t>(elem_kind),
                         static_cast<std::uint8_t>(metric), KNNG_MEM_HOST, 0};
   }
 };
+
+inline float cross_distance(const Dataset& a, std::size_t i, const Dataset& b, std::size_t j) {
+  if (a.elem_kind == ElemKind::f32)
+    return a.metric == MetricKind::l2
+               ? detail::l2_f32(a.f32.data() + i * a.dims, b.f32.data() + j * b.dims, a.dims)
+               : detail::cosine_t(a.f32.data() + i * a.dims, b.f32.data() + j * b.dims, a.dims);
+  return a.metric == MetricKind::l2
+             ? detail::l2_u8(a.u8.data() + i * a.dims, b.u8.data() + j * b.dims, a.dims)
+             : detail::cosine_t(a.u8.data() + i * a.dims, b.u8.data() + j * b.dims, a.dims);
+}
 
 struct NeighborEntry {
   PointId id = 0;
@@ -120,11 +249,47 @@ struct KnnGraph {
   }
   std::span<const PointId> ids_row(std::size_t r) const { return {ids.data() + r * k, k}; }
   std::span<const float> dists_row(std::size_t r) const { return {dists.data() + r * k, k}; }
+  std::span<PointId> ids_row(std::size_t r) { return {ids.data() + r * k, k}; }
+  std::span<float> dists_row(std::size_t r) { return {dists.data() + r * k, k}; }
+  std::vector<NeighborEntry> row_entries(std::size_t r) const {
+    std::vector<NeighborEntry> e(k);
+    for (std::size_t j = 0; j < k; ++j)
+      e[j] = {ids[r * k + j], dists[r * k + j], !flags.empty() && flags[r * k + j] != 0};
+    return e;
+  }
+  void set_row(std::size_t r, std::span<const NeighborEntry> e) {
+    if (e.size() != k) throw std::invalid_argument("KnnGraph::set_row: wrong row length");
+    for (std::size_t j = 0; j < k; ++j) {
+      ids[r * k + j] = e[j].id;
+      dists[r * k + j] = e[j].dist;
+      if (!flags.empty()) flags[r * k + j] = e[j].flag ? 1 : 0;
+    }
+  }
   knng_graph view() {
     return knng_graph{ids.data(), dists.data(), flags.empty() ? nullptr : flags.data(),
                       num_sources, k, KNNG_MEM_HOST, {0, 0, 0, 0, 0, 0, 0}};
   }
 };
+
+// check_graph_invariants core.cpp:166-186: shape, non-negative distances, no
+// self loop in local id space, rows sorted by (dist, id), no duplicate id.
+inline void check_graph_invariants(const KnnGraph& g) {
+  if (g.ids.size() != g.num_sources * g.k || g.dists.size() != g.ids.size())
+    throw std::logic_error("KnnGraph: matrix shape mismatch");
+  for (std::size_t r = 0; r < g.num_sources; ++r) {
+    const PointId* id = g.ids.data() + r * g.k;
+    const float* ds = g.dists.data() + r * g.k;
+    for (std::size_t j = 0; j < g.k; ++j) {
+      if (ds[j] < 0.0f) throw std::logic_error("KnnGraph: negative distance");
+      if (g.id_space == IdSpace::local && id[j] == r)
+        throw std::logic_error("KnnGraph: self-loop");
+      if (j && !(ds[j - 1] < ds[j] || (ds[j - 1] == ds[j] && id[j - 1] < id[j])))
+        throw std::logic_error("KnnGraph: row not sorted");
+      for (std::size_t m = j + 1; m < g.k; ++m)
+        if (id[m] == id[j]) throw std::logic_error("KnnGraph: duplicate id");
+    }
+  }
+}
 
 // merge_rows core.cpp:114-134 (on the GPU)
 inline std::vector<NeighborEntry> merge_rows(std::span<const NeighborEntry> a,
@@ -194,6 +359,7 @@ struct SearchGraph {
   std::span<const PointId> row(std::size_t r) const {
     return {ids.data() + r * out_degree, out_degree};
   }
+  std::span<PointId> row(std::size_t r) { return {ids.data() + r * out_degree, out_degree}; }
 };
 
 // optimize_graph graphopt.cpp:24-105 (bit-identical to the reference)
@@ -233,7 +399,7 @@ struct SearchResult {
   }
 };
 struct SearchDiagnostics {
-  bool collect_scored_ids = false;  // ids are not collected on the GPU; counts are
+  bool collect_scored_ids = false;  // scored ids in scoring order (second, exact pass)
   std::vector<std::vector<PointId>> scored_ids;
   std::vector<std::size_t> hops;
   std::vector<std::size_t> scored;
@@ -259,6 +425,20 @@ inline SearchResult ann_search(const Dataset& q, const SearchGraph& sg, const Da
   if (diag) {
     diag->hops.assign(hops.begin(), hops.end());
     diag->scored.assign(scored.begin(), scored.end());
+    diag->scored_ids.clear();
+    if (diag->collect_scored_ids) {
+      // the search is deterministic: rerun with the exact per-query capacity
+      std::uint64_t cap = 1;
+      for (auto c : scored) cap = std::max<std::uint64_t>(cap, c);
+      std::vector<std::uint32_t> ids(q.num_points * cap), h2(q.num_points), s2(q.num_points);
+      SearchResult r2 = r;
+      detail::check(knng_ann_search_scored_ids(
+          detail::ctx(), 0, &qd, sg.ids.empty() ? &kNoRow : sg.ids.data(), sg.num_sources,
+          sg.out_degree, &vd, &sp, KNNG_MEM_HOST, r2.ids.data(), r2.dists.data(), h2.data(),
+          s2.data(), ids.data(), cap));
+      for (std::size_t i = 0; i < q.num_points; ++i)
+        diag->scored_ids.emplace_back(ids.begin() + i * cap, ids.begin() + i * cap + s2[i]);
+    }
   }
   return r;
 }
@@ -356,11 +536,8 @@ struct DistBuildResult {
   std::vector<PhaseSnapshot> snapshots;
 };
 
-// build_distributed refine.cpp:504-586 (ranks on the context's GPUs)
-inline DistBuildResult build_distributed(const Dataset& d, const RefineConfig& cfg) {
-  DistBuildResult res;
-  res.graph = KnnGraph::allocate(d.num_points, cfg.k, IdSpace::global);
-  res.graph.flags.clear();
+namespace detail {
+inline knng_refine_config to_c(const RefineConfig& cfg) {
   knng_refine_config c{};
   c.ranks = cfg.ranks;
   c.groups = cfg.groups;
@@ -376,6 +553,25 @@ inline DistBuildResult build_distributed(const Dataset& d, const RefineConfig& c
   c.capture_snapshots = cfg.capture_snapshots;
   c.max_concat_bytes = cfg.max_concat_bytes;
   c.seed = cfg.seed;
+  return c;
+}
+inline std::vector<GetRecord> last_comm_log(std::uint64_t gets) {
+  std::vector<knng_get_record> recs(gets ? gets : 1);
+  std::uint64_t cnt = 0;
+  check(knng_last_comm_log(ctx(), recs.data(), recs.size(), &cnt));
+  std::vector<GetRecord> out;
+  for (std::uint64_t i = 0; i < cnt && i < recs.size(); ++i)
+    out.push_back({recs[i].src, recs[i].target, recs[i].region, recs[i].bytes, recs[i].epoch});
+  return out;
+}
+}  // namespace detail
+
+// build_distributed refine.cpp:504-586 (ranks on the context's GPUs)
+inline DistBuildResult build_distributed(const Dataset& d, const RefineConfig& cfg) {
+  DistBuildResult res;
+  res.graph = KnnGraph::allocate(d.num_points, cfg.k, IdSpace::global);
+  res.graph.flags.clear();
+  knng_refine_config c = detail::to_c(cfg);
   const knng_dataset ds = d.view();
   knng_graph gv = res.graph.view();
   knng_dist_result r{};
@@ -572,6 +768,7 @@ inline Dataset gen_random_dataset(std::size_t n, std::size_t dims, Distribution 
 
 struct GroundTruth {
   KnnGraph graph;
+  std::uint64_t dataset_hash = 0;
   std::size_t k = 0;
   MetricKind metric = MetricKind::l2;
 };
@@ -580,6 +777,7 @@ inline GroundTruth brute_force_knng(const Dataset& d, std::size_t k, std::size_t
   GroundTruth gt;
   gt.k = k;
   gt.metric = d.metric;
+  gt.dataset_hash = d.content_hash();
   gt.graph = KnnGraph::allocate(d.num_points, k, IdSpace::local);
   std::vector<std::uint64_t> rows(d.num_points);
   for (std::size_t i = 0; i < rows.size(); ++i) rows[i] = i;
@@ -643,3 +841,5 @@ inline KnnGraph load_graph(const std::filesystem::path& path, IdSpace space = Id
 }
 
 }  // namespace knng
+
+#include "knng_b200_host.hpp"

@@ -207,6 +207,18 @@ knng_status knng_ann_search(knng_ctx* ctx, int device, const knng_dataset* queri
                             const knng_dataset* vectors, const knng_search_params* params,
                             uint8_t out_mem, uint32_t* out_ids, float* out_dists,
                             uint32_t* hops, uint32_t* scored);
+/* ann_search with SearchDiagnostics::collect_scored_ids (annsearch.hpp:36-41):
+ * additionally writes each query's scored ids in scoring order into
+ * scored_ids[q * scored_cap ...] (the first min(scored[q], scored_cap) of
+ * them); hops and scored are required.  Call with the scored counts of a first
+ * knng_ann_search to size scored_cap exactly (the search is deterministic). */
+knng_status knng_ann_search_scored_ids(knng_ctx* ctx, int device, const knng_dataset* queries,
+                                       const uint32_t* sg_ids, uint64_t sg_n, uint64_t degree,
+                                       const knng_dataset* vectors,
+                                       const knng_search_params* params, uint8_t out_mem,
+                                       uint32_t* out_ids, float* out_dists, uint32_t* hops,
+                                       uint32_t* scored, uint32_t* scored_ids,
+                                       uint64_t scored_cap);
 
 /* search_throughput_probe annsearch.cpp:131-155 (ThroughputCase / Row,
  * annsearch.hpp:52-69): the batch search of `queries` against each case's
@@ -284,6 +296,27 @@ knng_status knng_build_distributed_rank(knng_ctx* ctx, int device, uint64_t rank
 knng_status knng_refine(knng_ctx* ctx, const float* x_perm, uint64_t n, uint64_t dims,
                         const knng_refine_config* cfg, const uint64_t* offsets, uint32_t* ids,
                         float* dists, int mode, knng_dist_result* result);
+/* The world-level phase drivers one at a time (refine.hpp:119-136,
+ * refine.cpp:430-502): phase 1 all_to_all_refine, 2 binary_tree_refine, 3
+ * grouped_merge, 4 flat_refine.  Each publishes what its phase needs (dataset + graph, or
+ * dataset + the rank's group search graph for flat_refine), barriers and runs
+ * its phase on every rank, like the reference's drivers on a caller-owned
+ * RankWorld: the world starts at epoch *epoch and *epoch receives its epoch at
+ * the end (the C++ drop-in's RankWorld carries it between calls).  ids/dists:
+ * n x k internal global ids, rank blocks at offsets, updated in place (phases
+ * 1, 2 and 4).  sg_in (phase 4) / sg_out (phase 3): per-rank blocks in rank order,
+ * block r = the search graph of rank r's group (group points x out_degree).
+ * The gets are in knng_last_comm_log. */
+knng_status knng_refine_phase(knng_ctx* ctx, const float* x_perm, uint64_t n, uint64_t dims,
+                              const knng_refine_config* cfg, const uint64_t* offsets, int phase,
+                              uint64_t* epoch, uint32_t* ids, float* dists,
+                              const uint32_t* sg_in, uint32_t* sg_out,
+                              knng_dist_result* result);
+/* effective_groups refine.cpp:160-183: the group count the refine phases use
+ * (cfg->groups, or P when skip_tree_phase is set or the max_concat_bytes
+ * footprint estimate is exceeded); offsets = P + 1 rank block bounds. */
+knng_status knng_effective_groups(const knng_refine_config* cfg, const uint64_t* offsets,
+                                  uint64_t dims, uint64_t* groups);
 /* Comm log of the last build_distributed / refine (RankWorld::comm_log). */
 knng_status knng_last_comm_log(knng_ctx* ctx, knng_get_record* records, uint64_t cap,
                                uint64_t* count);

@@ -600,11 +600,11 @@ knng_status knng_optimize_graph(knng_ctx* ctx, int device, const knng_graph* gph
   });
 }
 
-knng_status knng_ann_search(knng_ctx* ctx, int device, const knng_dataset* queries,
+static knng_status ann_search_impl(knng_ctx* ctx, int device, const knng_dataset* queries,
                             const uint32_t* sg_ids, uint64_t sg_n, uint64_t degree,
                             const knng_dataset* vectors, const knng_search_params* params,
                             uint8_t out_mem, uint32_t* out_ids, float* out_dists, uint32_t* hops,
-                            uint32_t* scored) {
+                            uint32_t* scored, uint32_t* scored_ids, uint64_t scored_cap) {
   return guard([&] {
     Runner& r = ctx->runner(device);
     DeviceGuard g(r.device);
@@ -630,13 +630,16 @@ knng_status knng_ann_search(knng_ctx* ctx, int device, const knng_dataset* queri
     const u64 ks = sp.k_s;
     if (out_mem == KNNG_MEM_DEVICE) {
       ann_search_device(r, q.p, nq, (int)queries->dims, sg, (u32)degree, v.p, vectors->n, sp, 0,
-                        out_ids, out_dists, hops, scored, nullptr, 0, q.nrm, v.nrm);
+                        out_ids, out_dists, hops, scored, nullptr, 0, q.nrm, v.nrm, scored_ids,
+                        scored_cap);
     } else {
       DBuf<u32> oi(r, nq * ks), hh(r, hops ? nq : 0), ss(r, scored ? nq : 0);
+      DBuf<u32> si(r, scored_ids ? nq * scored_cap : 0);
       DBuf<float> od(r, nq * ks);
       ann_search_device(r, q.p, nq, (int)queries->dims, sg, (u32)degree, v.p, vectors->n, sp, 0,
                         oi.p, od.p, hops ? hh.p : nullptr, scored ? ss.p : nullptr, nullptr, 0,
-                        q.nrm, v.nrm);
+                        q.nrm, v.nrm, scored_ids ? si.p : nullptr, scored_cap);
+      if (scored_ids) copy_out(r, scored_ids, si.p, nq * scored_cap, false);
       copy_out(r, out_ids, oi.p, nq * ks, false);
       copy_out(r, out_dists, od.p, nq * ks, false);
       if (hops) copy_out(r, hops, hh.p, nq, false);
@@ -645,6 +648,29 @@ knng_status knng_ann_search(knng_ctx* ctx, int device, const knng_dataset* queri
     }
     r.sync();
   });
+}
+
+knng_status knng_ann_search(knng_ctx* ctx, int device, const knng_dataset* queries,
+                            const uint32_t* sg_ids, uint64_t sg_n, uint64_t degree,
+                            const knng_dataset* vectors, const knng_search_params* params,
+                            uint8_t out_mem, uint32_t* out_ids, float* out_dists, uint32_t* hops,
+                            uint32_t* scored) {
+  return ann_search_impl(ctx, device, queries, sg_ids, sg_n, degree, vectors, params, out_mem,
+                         out_ids, out_dists, hops, scored, nullptr, 0);
+}
+
+knng_status knng_ann_search_scored_ids(knng_ctx* ctx, int device, const knng_dataset* queries,
+                                       const uint32_t* sg_ids, uint64_t sg_n, uint64_t degree,
+                                       const knng_dataset* vectors,
+                                       const knng_search_params* params, uint8_t out_mem,
+                                       uint32_t* out_ids, float* out_dists, uint32_t* hops,
+                                       uint32_t* scored, uint32_t* scored_ids,
+                                       uint64_t scored_cap) {
+  if (!scored_ids || !scored) return ann_search_impl(ctx, device, queries, sg_ids, sg_n, degree,
+                                                     vectors, params, out_mem, out_ids, out_dists,
+                                                     hops, scored, nullptr, 0);
+  return ann_search_impl(ctx, device, queries, sg_ids, sg_n, degree, vectors, params, out_mem,
+                         out_ids, out_dists, hops, scored, scored_ids, scored_cap);
 }
 
 knng_status knng_search_throughput_probe(knng_ctx* ctx, int device,
@@ -890,6 +916,33 @@ knng_status knng_refine(knng_ctx* ctx, const float* x_perm, uint64_t n, uint64_t
     refine_from_local(ctx->devices, x_perm, n, (int)dims, c, off, ids, dists, mode, &res);
     ctx->last_log = res.comm_log;
     fill_dist_result(res, result);
+  });
+}
+
+knng_status knng_refine_phase(knng_ctx* ctx, const float* x_perm, uint64_t n, uint64_t dims,
+                              const knng_refine_config* cfg, const uint64_t* offsets, int phase,
+                              uint64_t* epoch, uint32_t* ids, float* dists,
+                              const uint32_t* sg_in, uint32_t* sg_out,
+                              knng_dist_result* result) {
+  return guard([&] {
+    require(ctx && x_perm && cfg && offsets && ids && dists && epoch, "refine: null argument");
+    const RefineCfg c = to_cfg(cfg);
+    std::vector<uint64_t> off(offsets, offsets + c.ranks + 1);
+    DistResult res;
+    refine_phase(ctx->devices, x_perm, n, (int)dims, c, off, phase, *epoch, ids, dists, sg_in,
+                 sg_out, &res, epoch);
+    ctx->last_log = res.comm_log;
+    fill_dist_result(res, result);
+  });
+}
+
+knng_status knng_effective_groups(const knng_refine_config* cfg, const uint64_t* offsets,
+                                  uint64_t dims, uint64_t* groups) {
+  return guard([&] {
+    require(cfg && offsets && groups, "effective_groups: null argument");
+    const RefineCfg c = to_cfg(cfg);
+    std::vector<uint64_t> off(offsets, offsets + c.ranks + 1);
+    *groups = effective_group_count(off, c, (int)dims);
   });
 }
 

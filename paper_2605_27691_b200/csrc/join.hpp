@@ -35,6 +35,7 @@ struct JoinLaunch {
   const float* X = nullptr;
   const float* nrm = nullptr;  // cosine norm chains (null: l2)
   int d = 0;
+  uint64_t n_rows = 0;  // rows of X (the tensor-core join's TMA map)
   const uint32_t* L_ids = nullptr;
   const uint32_t* L_cnt = nullptr;
   const float* worst = nullptr;
@@ -49,6 +50,14 @@ struct JoinLaunch {
 };
 
 void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& a);
+
+// Tensor-core join (join_tc.cu): tf32 Gram of the centred list rows decides,
+// offers carry a lower bound of the exact distance (k_apply recomputes the
+// exact distance of every candidate it may insert).  l2, d % 4 == 0, lists of
+// <= 128 rows; opt-in with KNNG_JOIN=tc (the exact-order kernel above is the
+// default: it measured faster).
+bool join_tc_supported(const float* X, int d, uint32_t k, uint32_t B, bool cosine);
+void launch_join_tc(const Runner& r, const JoinPlan& plan, const JoinLaunch& a);
 
 // act[0 .. off[n]) = the points whose join descriptor is non-empty (a new
 // entry exists), ascending; flag/off are scratch (n and n + 1 entries).

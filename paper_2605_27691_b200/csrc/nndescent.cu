@@ -308,11 +308,16 @@ __global__ __launch_bounds__(256) void k_rev_select(u64 n, u32 B, u64 iter_seed,
 // ---------------------------------------------------------------------------
 // apply_candidates nndescent.cpp:199-223 -- warp per point
 // ---------------------------------------------------------------------------
+// With X set the buckets hold LOWER BOUNDS of the exact distances (the
+// tensor-core join, join_tc.cu): every candidate whose bound beats the row's
+// current worst gets its exact-order distance recomputed here (core.hpp:23-30),
+// so the inserted keys -- and the decisions of knn_insert -- are exact.
 __global__ __launch_bounds__(256) void k_apply(u64 n, u32 k, u32 S, u64* __restrict__ keys,
                                                u32* __restrict__ flags,
                                                float* __restrict__ worst,
                                                u64* __restrict__ slots,
-                                               u64* __restrict__ counters) {
+                                               u64* __restrict__ counters,
+                                               const float* __restrict__ X, int d) {
   const unsigned lane = lane_id();
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
   u64 acc_total = 0;
@@ -336,11 +341,16 @@ __global__ __launch_bounds__(256) void k_apply(u64 n, u32 k, u32 S, u64* __restr
         fl = (flags[p] >> lane) & 1u;
         last = __shfl_sync(kFull, rk, k - 1);
       }
-      mask = __ballot_sync(kFull, filled && s < last);
+      u64 sx = s;
+      if (X && filled && s < last) {
+        const u32 v = key_id(s);
+        sx = pack_key(l2_exact(X + p * (u64)d, X + (u64)v * d, d), v);
+      }
+      mask = __ballot_sync(kFull, filled && sx < last);
       while (mask) {
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
-        const u64 c = __shfl_sync(kFull, s, src);
+        const u64 c = __shfl_sync(kFull, sx, src);
         // knn_insert core.cpp:99-112: reject duplicates and non-improvements
         if (c >= last) continue;
         if (__ballot_sync(kFull, lane < k && key_id(rk) == key_id(c))) continue;
@@ -645,6 +655,8 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   jl.X = ds.x;
   jl.nrm = ds.nrm;
   jl.d = ds.d;
+  jl.n_rows = n;
+  const bool use_tc = join_tc_supported(ds.x, ds.d, k, B, ds.nrm != nullptr);
   jl.L_ids = L_ids_p;
   jl.L_cnt = L_cnt.p;
   jl.worst = worst.p;
@@ -683,7 +695,12 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
       jl.p_hi = std::min<u64>(n, jl.p_lo + slice);
       chunk_ctr.zero();
       tm.tick(kStLists);
-      launch_join(r, plan, jl);
+      if (use_tc) {
+        q_fill.zero();
+        launch_join_tc(r, plan, jl);
+      } else {
+        launch_join(r, plan, jl);
+      }
       tm.tick(kStJoin);
       launch_offer(r, plan, q_key_p, q_tgt_p, q_fill.p,
                    (u32)ceil_div<u64>(jl.p_hi - jl.p_lo, (u64)kJoinChunk), slots_p, S, nb, ways,
@@ -692,7 +709,7 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
       launches += 2;
     }
     k_apply<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst.p, slots_p,
-                                                   counters.p);
+                                                   counters.p, use_tc ? ds.x : nullptr, ds.d);
     KNNG_LAUNCH_CHECK();
     launches += 1;
     tm.tick(kStApply);

@@ -122,6 +122,10 @@ DBuf<float> norms_of(const Shared& S, Runner& r, const float* x, uint64_t n) {
 void pull_rows(Shared& S, RankState& R, uint64_t j, const char* name, void* dst) {
   S.world->get(R.rank, j, name, dst, *R.runner);
 }
+// the same pull, issued on another stream of the rank's device
+void pull_rows_on(Shared& S, RankState& R, uint64_t j, const char* name, void* dst, Runner& on) {
+  S.world->get(R.rank, j, name, dst, on);
+}
 
 // search the local points against (sg, vectors) and fold results into the
 // rank's graph (refine.cpp:212-214, 332-333)
@@ -184,7 +188,9 @@ void tree_level(Shared& S, RankState& R, uint64_t level, DBuf<float>& span_x, ui
   S.world->barrier(R.rank, r);
 }
 
-// grouped_merge_rank refine.cpp:256-293; returns the group search graph
+// grouped_merge_rank refine.cpp:256-293; returns the group search graph.
+// span_x == nullptr: the standalone driver (refine.cpp:272-283) -- the
+// members' datasets are pulled too (graph then dataset per member).
 DBuf<u32> grouped_merge(Shared& S, RankState& R, const float* span_x, uint64_t span_n) {
   Runner& r = *R.runner;
   const uint64_t p = S.offsets.size() - 1;
@@ -192,16 +198,25 @@ DBuf<u32> grouped_merge(Shared& S, RankState& R, const float* span_x, uint64_t s
   const uint64_t glo = (R.rank / gsz) * gsz, ghi = glo + gsz;
   const uint64_t base = S.offsets[glo];
   const uint64_t cnt = S.offsets[ghi] - base;
-  require(cnt == span_n, "grouped_merge: span/group size mismatch");
+  DBuf<float> group_x;
+  if (!span_x) group_x.alloc(r, cnt * S.d);
+  require(!span_x || cnt == span_n, "grouped_merge: span/group size mismatch");
   DBuf<u64> concat(r, cnt * S.k);
   for (uint64_t j = glo; j < ghi; ++j) {
     u64* dst = concat.p + (S.offsets[j] - base) * S.k;
-    if (j == R.rank)
+    float* xdst = span_x ? nullptr : group_x.p + (S.offsets[j] - base) * S.d;
+    if (j == R.rank) {
       KNNG_CUDA(cudaMemcpyAsync(dst, R.keys.p, R.n_local * S.k * 8, cudaMemcpyDeviceToDevice,
                                 r.stream));
-    else
+      if (xdst)
+        KNNG_CUDA(cudaMemcpyAsync(xdst, R.local_x.p, R.n_local * S.d * 4,
+                                  cudaMemcpyDeviceToDevice, r.stream));
+    } else {
       pull_rows(S, R, j, kGraph, dst);
+      if (xdst) pull_rows(S, R, j, kDataset, xdst);
+    }
   }
+  if (!span_x) span_x = group_x.p;
   DBuf<u32> gs(r, cnt * S.od);
   {
     const DBuf<float> sn = norms_of(S, r, span_x, cnt);
@@ -215,9 +230,12 @@ DBuf<u32> grouped_merge(Shared& S, RankState& R, const float* span_x, uint64_t s
 }
 
 // flat_refine_rank refine.cpp:300-351
+void flat_refine_double_buffered(Shared& S, RankState& R);
+
 void flat_refine(Shared& S, RankState& R) {
   Runner& r = *R.runner;
   if (S.groups <= 1) return;
+  if (S.cfg->double_buffer && S.groups > 2) return flat_refine_double_buffered(S, R);
   const uint64_t p = S.offsets.size() - 1;
   const uint64_t gsz = p / S.groups;
   const uint64_t my_group = R.rank / gsz, pos = R.rank % gsz;
@@ -232,6 +250,64 @@ void flat_refine(Shared& S, RankState& R) {
     for (uint64_t j = grp * gsz; j < (grp + 1) * gsz; ++j)
       pull_rows(S, R, j, kDataset, vx.p + (S.offsets[j] - base) * S.d);
     search_and_merge(S, R, sg.p, vx.p, cnt, base);
+  }
+  r.sync();
+}
+
+// double_buffer (refine.cpp:343-350): the next group's pulls (its search graph
+// from the same-position rank + the member datasets, one-sided copies over
+// NVLink) run on a second stream while the current group is searched; two
+// buffer sets alternate, each reused only after the search that read it is
+// done.  Same gets, same results -- only the overlap differs.
+void flat_refine_double_buffered(Shared& S, RankState& R) {
+  Runner& r = *R.runner;
+  const uint64_t p = S.offsets.size() - 1;
+  const uint64_t gsz = p / S.groups;
+  const uint64_t my_group = R.rank / gsz, pos = R.rank % gsz;
+  uint64_t max_cnt = 0;
+  for (uint64_t g = 0; g < S.groups; ++g)
+    max_cnt = std::max<uint64_t>(max_cnt, S.offsets[(g + 1) * gsz] - S.offsets[g * gsz]);
+  DBuf<u32> sg[2] = {DBuf<u32>(r, max_cnt * S.od), DBuf<u32>(r, max_cnt * S.od)};
+  DBuf<float> vx[2] = {DBuf<float>(r, max_cnt * S.d), DBuf<float>(r, max_cnt * S.d)};
+  cudaStream_t side_s = nullptr;
+  KNNG_CUDA(cudaStreamCreateWithFlags(&side_s, cudaStreamNonBlocking));
+  cudaEvent_t landed[2], freed[2];
+  for (int b = 0; b < 2; ++b) {
+    KNNG_CUDA(cudaEventCreateWithFlags(&landed[b], cudaEventDisableTiming));
+    KNNG_CUDA(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
+    KNNG_CUDA(cudaEventRecord(freed[b], r.stream));  // buffers allocated on r.stream
+  }
+  struct Cleanup {
+    cudaStream_t s;
+    cudaEvent_t* e;
+    ~Cleanup() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+      for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+    }
+  };
+  cudaEvent_t evs[4] = {landed[0], landed[1], freed[0], freed[1]};
+  Cleanup cleanup{side_s, evs};
+  Runner side(r.device, side_s);
+  auto fetch = [&](uint64_t step, int b) {
+    const uint64_t grp = (my_group + step) % S.groups;
+    const uint64_t base = S.offsets[grp * gsz];
+    KNNG_CUDA(cudaStreamWaitEvent(side_s, freed[b], 0));
+    pull_rows_on(S, R, grp * gsz + pos, kSGraph, sg[b].p, side);
+    for (uint64_t j = grp * gsz; j < (grp + 1) * gsz; ++j)
+      pull_rows_on(S, R, j, kDataset, vx[b].p + (S.offsets[j] - base) * S.d, side);
+    KNNG_CUDA(cudaEventRecord(landed[b], side_s));
+  };
+  fetch(1, 0);
+  for (uint64_t step = 1; step < S.groups; ++step) {
+    const int b = (int)((step - 1) & 1);
+    if (step + 1 < S.groups) fetch(step + 1, b ^ 1);
+    const uint64_t grp = (my_group + step) % S.groups;
+    const uint64_t base = S.offsets[grp * gsz];
+    const uint64_t cnt = S.offsets[(grp + 1) * gsz] - base;
+    KNNG_CUDA(cudaStreamWaitEvent(r.stream, landed[b], 0));
+    search_and_merge(S, R, sg[b].p, vx[b].p, cnt, base);
+    KNNG_CUDA(cudaEventRecord(freed[b], r.stream));
   }
   r.sync();
 }
@@ -424,6 +500,11 @@ void fill_result(Shared& S, std::vector<RankState>& ranks, World* world, DistRes
 
 }  // namespace
 
+uint64_t effective_group_count(const std::vector<uint64_t>& offsets, const RefineCfg& cfg,
+                               int d) {
+  return effective_groups(offsets, cfg, d);
+}
+
 uint64_t tree_levels(uint64_t ranks, uint64_t groups) {
   require(is_pow2(ranks) && is_pow2(groups) && groups <= ranks, "tree_levels: invalid P or M");
   return log2_exact(ranks / groups);
@@ -591,6 +672,120 @@ void refine_from_local(const std::vector<int>& devices, const float* X_perm, uin
   fill_result(S, ranks, &world, res);
 }
 
+// The world-level phase drivers one at a time (refine.cpp:430-502): each
+// publishes what its phase needs, barriers, and runs its phase on every rank.
+//   phase 1 all_to_all_refine:  ids/dists in/out
+// The world starts at epoch `epoch0` (the caller's RankWorld may have run
+// earlier drivers); `epoch_out` receives its epoch at the end.
+//   phase 2 binary_tree_refine: ids/dists in/out
+//   phase 3 grouped_merge:      sg_out[rank block] = the rank's group search graph
+//   phase 4 flat_refine:        sg_in[rank block] = group_graphs[rank]; ids/dists in/out
+// sg blocks: rank r's block holds group_n(r) x out_degree ids, blocks in rank order.
+void refine_phase(const std::vector<int>& devices, const float* X_perm, uint64_t n, int d,
+                  const RefineCfg& cfg, const std::vector<uint64_t>& offsets, int phase,
+                  uint64_t epoch0, uint32_t* ids, float* dists, const uint32_t* sg_in,
+                  uint32_t* sg_out, DistResult* res, uint64_t* epoch_out) {
+  require(!devices.empty(), "refine: no CUDA device");
+  require(offsets.size() == cfg.ranks + 1 && offsets.back() == n, "refine: bad offsets");
+  require(phase >= 1 && phase <= 4, "refine: unknown phase");
+  validate_config(offsets, cfg);
+  Shared S = make_shared_state(cfg, offsets, d);
+  const uint64_t p = cfg.ranks;
+  const uint64_t gsz = p / S.groups;
+  auto group_n = [&](uint64_t r) {
+    const uint64_t glo = (r / gsz) * gsz;
+    return S.offsets[glo + gsz] - S.offsets[glo];
+  };
+  std::vector<uint64_t> sg_off(p + 1, 0);
+  for (uint64_t r = 0; r < p; ++r) sg_off[r + 1] = sg_off[r] + group_n(r) * S.od;
+  require(phase <= 2 || (phase == 3 ? sg_out != nullptr : sg_in != nullptr),
+          "refine: search-graph buffer expected");
+  std::vector<RankState> ranks(p);
+  for (uint64_t i = 0; i < p; ++i) {
+    RankState& R = ranks[i];
+    R.rank = i;
+    R.runner = owned_runner(devices[i % devices.size()]);
+    Runner& r = *R.runner;
+    DeviceGuard g(r.device);
+    R.n_local = size_of(S, i);
+    R.local_x.alloc(r, R.n_local * d);
+    R.keys.alloc(r, R.n_local * S.k);
+    KNNG_CUDA(cudaMemcpyAsync(R.local_x.p, X_perm + offsets[i] * d, R.n_local * d * 4,
+                              cudaMemcpyHostToDevice, r.stream));
+    DBuf<u32> ti(r, R.n_local * S.k);
+    DBuf<float> td(r, R.n_local * S.k);
+    KNNG_CUDA(cudaMemcpyAsync(ti.p, ids + offsets[i] * S.k, R.n_local * S.k * 4,
+                              cudaMemcpyHostToDevice, r.stream));
+    KNNG_CUDA(cudaMemcpyAsync(td.p, dists + offsets[i] * S.k, R.n_local * S.k * 4,
+                              cudaMemcpyHostToDevice, r.stream));
+    import_graph_device(r, ti.p, td.p, nullptr, R.n_local, (u32)S.k, R.keys.p, nullptr);
+    r.sync();
+  }
+  ThreadWorld world(p, std::chrono::seconds(600), epoch0);
+  S.world = &world;
+  run_ranks(world, p, [&](size_t i) {
+    RankState& R = ranks[i];
+    Runner& r = *R.runner;
+    DeviceGuard g(r.device);
+    if (phase == 1) {  // all_to_all_refine publishes and barriers itself
+      const double t = now_s();
+      a2a_refine(S, R);
+      R.flat_t = now_s() - t;
+      return;
+    }
+    S.world->publish(R.rank, kDataset, R.local_x.p, R.n_local * S.d * 4,
+                     wire_region_size(RegionKind::dataset, R.n_local, S.d, S.cfg->u8_elems), r);
+    if (phase == 4) {
+      const uint64_t cnt = group_n(i);
+      DBuf<u32> gs(r, cnt * S.od);
+      KNNG_CUDA(cudaMemcpyAsync(gs.p, sg_in + sg_off[i], cnt * S.od * 4, cudaMemcpyHostToDevice,
+                                r.stream));
+      S.world->publish(R.rank, kSGraph, gs.p, cnt * S.od * 4,
+                       wire_region_size(RegionKind::sgraph, cnt, S.od), r);
+    } else {
+      S.world->publish(R.rank, kGraph, R.keys.p, R.n_local * S.k * 8,
+                       wire_region_size(RegionKind::knng, R.n_local, S.k), r);
+    }
+    S.world->barrier(R.rank, r);
+    const double t = now_s();
+    if (phase == 2) {
+      DBuf<float> span_x(r, R.n_local * S.d);
+      KNNG_CUDA(cudaMemcpyAsync(span_x.p, R.local_x.p, R.n_local * S.d * 4,
+                                cudaMemcpyDeviceToDevice, r.stream));
+      uint64_t span_lo = S.offsets[R.rank], span_n = R.n_local;
+      for (uint64_t level = 0; level < S.levels; ++level)
+        tree_level(S, R, level, span_x, span_lo, span_n);
+      r.sync();
+      R.tree_t = now_s() - t;
+    } else if (phase == 3) {
+      DBuf<u32> gs = grouped_merge(S, R, nullptr, 0);
+      KNNG_CUDA(cudaMemcpyAsync(sg_out + sg_off[i], gs.p, group_n(i) * S.od * 4,
+                                cudaMemcpyDeviceToHost, r.stream));
+      r.sync();
+      R.merge_t = now_s() - t;
+    } else {
+      flat_refine(S, R);
+      R.flat_t = now_s() - t;
+    }
+  });
+  if (phase != 3) {
+    for (auto& R : ranks) {
+      Runner& r = *R.runner;
+      DeviceGuard g(r.device);
+      DBuf<u32> ti(r, R.n_local * S.k);
+      DBuf<float> td(r, R.n_local * S.k);
+      export_graph_device(r, R.keys.p, nullptr, R.n_local, (u32)S.k, 0, ti.p, td.p, nullptr);
+      KNNG_CUDA(cudaMemcpyAsync(ids + offsets[R.rank] * S.k, ti.p, R.n_local * S.k * 4,
+                                cudaMemcpyDeviceToHost, r.stream));
+      KNNG_CUDA(cudaMemcpyAsync(dists + offsets[R.rank] * S.k, td.p, R.n_local * S.k * 4,
+                                cudaMemcpyDeviceToHost, r.stream));
+      r.sync();
+    }
+  }
+  fill_result(S, ranks, &world, res);
+  if (epoch_out) *epoch_out = world.epoch();
+}
+
 uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const HostTransport& t,
                                 const float* X, bool x_on_device, uint64_t n, int d,
                                 const RefineCfg& cfg_in, uint32_t* out_ids, float* out_dists,
@@ -649,8 +844,19 @@ uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const Hos
     world = std::make_unique<ProcWorld>(ranks, rank, t);
     S.world = world.get();
   }
-  local_build_rank(S, cfg, R);
-  if (ranks > 1) refine_rank(S, R, false);
+  try {
+    local_build_rank(S, cfg, R);
+    // failure injection for the abort-propagation test (tests/test_multiprocess_gpu.py)
+    if (const char* f = std::getenv("KNNG_INJECT_FAIL_RANK"))
+      if (std::atoi(f) == (int)rank)
+        throw std::runtime_error("injected failure at rank " + std::to_string(rank));
+    if (ranks > 1) refine_rank(S, R, false);
+  } catch (const std::exception& e) {
+    // a failing rank aborts the world so that its peers' barriers return
+    // WorldAborted instead of waiting for it (RankRunner distsim.hpp:127-129)
+    if (world) world->abort("rank " + std::to_string(rank) + " failed: " + e.what());
+    throw;
+  }
   const double te = now_s();
   if (out_on_device) {
     translate_rows_device(r, R.keys.p, R.n_local, (u32)S.k, to_ext.p, offsets[rank], out_ids,

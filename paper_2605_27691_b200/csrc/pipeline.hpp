@@ -45,6 +45,10 @@ struct DistResult {
   std::vector<std::vector<float>> snap_dists;
 };
 
+// effective_groups refine.cpp:160-183: M, or P when the tree phase is skipped
+// (skip_tree_phase, or the max_concat_bytes estimate exceeded).
+uint64_t effective_group_count(const std::vector<uint64_t>& offsets, const RefineCfg& cfg, int d);
+
 // Tree schedule helpers (refine.cpp:128-149).
 uint64_t tree_levels(uint64_t ranks, uint64_t groups);
 struct TreeLevel {
@@ -80,5 +84,13 @@ uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const Hos
 void refine_from_local(const std::vector<int>& devices, const float* X_perm, uint64_t n, int d,
                        const RefineCfg& cfg, const std::vector<uint64_t>& offsets, uint32_t* ids,
                        float* dists, int mode, DistResult* res);
+
+// One world-level phase driver (1 all_to_all_refine, 2 binary_tree_refine,
+// 3 grouped_merge, 4 flat_refine, refine.cpp:430-502) on a world starting at epoch `epoch0`.
+// sg_in / sg_out: per-rank blocks (group_n(rank) x out_degree), rank order.
+void refine_phase(const std::vector<int>& devices, const float* X_perm, uint64_t n, int d,
+                  const RefineCfg& cfg, const std::vector<uint64_t>& offsets, int phase,
+                  uint64_t epoch0, uint32_t* ids, float* dists, const uint32_t* sg_in,
+                  uint32_t* sg_out, DistResult* res, uint64_t* epoch_out);
 
 }  // namespace knng_b200

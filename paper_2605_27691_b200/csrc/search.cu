@@ -72,6 +72,8 @@ struct SearchArgs {
   float* out_d;
   u32* hops_out;
   u32* scored_out;
+  u32* scored_ids;   // diagnostics: ids in scoring order, scored_cap per query (null: off)
+  u64 scored_cap;
   u64* gtable;  // per-CTA tagged visited tables (gcap slots each), may be null
   u32 gcap;
   u64* counters;  // [0] hops [1] scored [2] overflowed queries / cache resets
@@ -418,6 +420,14 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
       const u64 c = score_batch<kCos>(a, s_q, s_stage, s_ptr, id, take, qnorm);
       beam_merge(c, s_beam, s_flag, s_clo, bs, W);
     };
+    // SearchDiagnostics::scored_ids (annsearch.hpp:36-41): every scored id in
+    // scoring order (exact mode only: no id is ever scored twice)
+    auto record = [&](u32 id, bool take) {
+      if (!a.scored_ids) return;
+      const unsigned tb = __ballot_sync(kFull, take);
+      const u32 pos = scored + __popc(tb & lanemask_lt());
+      if (take && pos < a.scored_cap) a.scored_ids[q * a.scored_cap + pos] = id;
+    };
 
     // entry points: sample_distinct(n, entries, Rng(mix_seed(seed, 0xa11ce000+q)))
     // (host sizes the cache so it never re-seeds before the entries are drawn)
@@ -427,6 +437,7 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
         const bool take = id < a.nv;
         if (take) vis.insert((u32)id);
         const u32 nt = __popc(__ballot_sync(kFull, take));
+        record((u32)id, take);
         after_insert(nt);
         score_and_merge((u32)id, take);
         scored += nt;
@@ -447,6 +458,7 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
         if (take) vis.insert(x);
         const u32 ntake = __popc(__ballot_sync(kFull, take));
         got += ntake;
+        record(x, take);
         scored += ntake;
         after_insert(ntake);
         score_and_merge(x, take);
@@ -483,6 +495,7 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
           fresh = cand && vis.insert(nb);
         }
         const u32 nf = __popc(__ballot_sync(kFull, fresh));
+        record(nb, fresh);
         scored += nf;
         if (!a.cache) after_insert(nf);
         score_and_merge(nb, fresh);
@@ -580,7 +593,8 @@ void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint
                        uint32_t deg, const float* V, uint64_t nv, const SearchParamsDev& p,
                        uint32_t id_base, uint32_t* out_ids, float* out_d, uint32_t* hops,
                        uint32_t* scored, SearchCounters* counters, uint64_t qbase,
-                       const float* qn, const float* vn) {
+                       const float* qn, const float* vn, uint32_t* scored_ids,
+                       uint64_t scored_cap) {
   require((qn == nullptr) == (vn == nullptr), "ann_search: cosine needs both norm arrays");
   validate_search((uint64_t)d, (uint64_t)d, nv, nv, p);
   if (nq == 0) return;
@@ -591,7 +605,8 @@ void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint
   if (entries > nv) entries = nv;
 
   // per-query diagnostics mirror the reference's exact visited-set size
-  const bool exact = scored != nullptr || getenv("KNNG_SEARCH_EXACT") != nullptr;
+  const bool exact =
+      scored != nullptr || scored_ids != nullptr || getenv("KNNG_SEARCH_EXACT") != nullptr;
   const SearchShape sh = search_shape(d, width, entries, exact);
   KNNG_CUDA(cudaFuncSetAttribute(k_search<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sh.smem));
@@ -622,6 +637,8 @@ void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint
   a.out_d = out_d;
   a.hops_out = hops;
   a.scored_out = scored;
+  a.scored_ids = scored_ids;
+  a.scored_cap = scored_cap;
   a.id_base = id_base;
   a.vis_slots = sh.vis_slots;
   a.vis_limit = sh.vis_limit;

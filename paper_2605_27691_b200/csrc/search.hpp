@@ -33,6 +33,7 @@ void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint
                        uint32_t deg, const float* V, uint64_t nv, const SearchParamsDev& p,
                        uint32_t id_base, uint32_t* out_ids, float* out_d, uint32_t* hops,
                        uint32_t* scored, SearchCounters* counters, uint64_t qbase = 0,
-                       const float* qn = nullptr, const float* vn = nullptr);  // cosine norms
+                       const float* qn = nullptr, const float* vn = nullptr,  // cosine norms
+                       uint32_t* scored_ids = nullptr, uint64_t scored_cap = 0);
 
 }  // namespace knng_b200

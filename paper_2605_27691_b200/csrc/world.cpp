@@ -9,6 +9,9 @@
 #include <mutex>
 #include <utility>
 #include <vector>
+#include <thread>
+#include <condition_variable>
+#include <memory>
 
 namespace knng_b200 {
 
@@ -26,6 +29,12 @@ struct RegionCache {
   };
   std::mutex mu;
   std::vector<Entry> free_list;
+  // buffers ever exported through a CUDA IPC handle (ProcWorld): peers may
+  // still hold a mapping of them, and freeing an allocation that another
+  // process has mapped is undefined, so these are never returned to the
+  // driver (they are reused by best fit build after build; their set is
+  // bounded by the largest build's regions)
+  std::vector<void*> exported;
   static constexpr uint64_t kMaxCachedPerDev = uint64_t{24} << 30;
 
   void* acquire(int dev, uint64_t bytes, uint64_t* got) {
@@ -64,7 +73,9 @@ struct RegionCache {
         if (e.dev == dev) total += e.bytes;
       // over the cap: drop the oldest entries of this device
       for (size_t i = 0; i < free_list.size() && total > kMaxCachedPerDev;) {
-        if (free_list[i].dev == dev) {
+        const bool pinned_by_peers =
+            std::find(exported.begin(), exported.end(), free_list[i].p) != exported.end();
+        if (free_list[i].dev == dev && !pinned_by_peers) {
           total -= free_list[i].bytes;
           evict.push_back(free_list[i]);
           free_list.erase(free_list.begin() + (std::ptrdiff_t)i);
@@ -84,9 +95,18 @@ struct RegionCache {
   }
 };
 
+void mark_exported(void* p);
+
 RegionCache& region_cache() {
   static RegionCache* c = new RegionCache();  // process lifetime (freed by the driver at exit)
   return *c;
+}
+
+void mark_exported(void* p) {
+  RegionCache& c = region_cache();
+  std::lock_guard<std::mutex> l(c.mu);
+  if (std::find(c.exported.begin(), c.exported.end(), p) == c.exported.end())
+    c.exported.push_back(p);
 }
 
 // Imported IPC mappings, process-wide: the exporting ranks keep their region
@@ -137,8 +157,8 @@ uint64_t wire_region_size(RegionKind kind, uint64_t rows, uint64_t cols, bool u8
   return header;
 }
 
-ThreadWorld::ThreadWorld(size_t num_ranks, std::chrono::milliseconds watchdog)
-    : num_ranks_(num_ranks), watchdog_(watchdog) {
+ThreadWorld::ThreadWorld(size_t num_ranks, std::chrono::milliseconds watchdog, uint64_t epoch0)
+    : num_ranks_(num_ranks), watchdog_(watchdog), epoch_(epoch0) {
   require(num_ranks >= 1, "RankWorld: P must be >= 1");
 }
 
@@ -294,7 +314,9 @@ std::vector<GetRecord> ThreadWorld::comm_log() const {
 // ProcWorld
 // ---------------------------------------------------------------------------
 ProcWorld::ProcWorld(size_t num_ranks, size_t rank, const HostTransport& t)
-    : num_ranks_(num_ranks), rank_(rank), t_(t) {
+    : num_ranks_(num_ranks), rank_(rank), watchdog_(std::chrono::seconds(600)), t_(t) {
+  if (const char* v = std::getenv("KNNG_WORLD_WATCHDOG_S"))
+    watchdog_ = std::chrono::milliseconds((long long)(std::atof(v) * 1000.0));
   require(num_ranks >= 1 && rank < num_ranks, "RankWorld: rank out of range");
   require(t.allgather != nullptr, "RankWorld: the process transport needs an allgather");
   remote_.assign(num_ranks, {});
@@ -307,11 +329,40 @@ ProcWorld::~ProcWorld() {
   }
 }
 
+// The caller's all-gather on a helper thread, waited on with the watchdog: a
+// peer that never arrives (crashed, hung, mismatched barrier counts) turns into
+// a WorldError here instead of a hang.  On a timeout the helper is left
+// blocked in the transport (it owns its buffers) and the world is dead.
 void ProcWorld::allgather(const void* in, uint64_t bytes, void* out) {
-  if (t_.allgather(t_.user, in, bytes, out) != 0) {
-    aborted_ = true;
+  if (transport_dead_) throw WorldAborted("RankWorld: aborted (transport closed)");
+  struct Call {
+    std::vector<unsigned char> in, out;
+    int rc = -1;
+    bool done = false;
+    std::mutex mu;
+    std::condition_variable cv;
+  };
+  auto c = std::make_shared<Call>();
+  c->in.assign(static_cast<const unsigned char*>(in), static_cast<const unsigned char*>(in) + bytes);
+  c->out.resize(bytes * num_ranks_);
+  HostTransport t = t_;
+  std::thread([c, t] {
+    const int rc = t.allgather(t.user, c->in.data(), c->in.size(), c->out.data());
+    std::lock_guard<std::mutex> l(c->mu);
+    c->rc = rc;
+    c->done = true;
+    c->cv.notify_all();
+  }).detach();
+  std::unique_lock<std::mutex> l(c->mu);
+  if (!c->cv.wait_for(l, watchdog_, [&] { return c->done; })) {
+    aborted_ = transport_dead_ = true;
+    throw WorldError("barrier watchdog timeout at rank " + std::to_string(rank_));
+  }
+  if (c->rc != 0) {
+    aborted_ = transport_dead_ = true;
     throw WorldAborted("RankWorld: host transport failed (another rank aborted?)");
   }
+  std::memcpy(out, c->out.data(), c->out.size());
 }
 
 void ProcWorld::publish(size_t rank, const std::string& name, const void* dev_ptr,
@@ -356,7 +407,19 @@ void ProcWorld::barrier(size_t rank, Runner& r) {
     }
   }
   ++epoch_;
-  // exchange the tables of current regions (the all-gather is the barrier)
+  exchange_tables(0, std::string());
+}
+
+// One barrier exchange: Control + the tables of current regions, all-gathered
+// (the all-gather is the barrier).
+void ProcWorld::exchange_tables(int aborted, const std::string& reason) {
+  constexpr size_t kBlock = sizeof(Control) + sizeof(Entry) * kMaxRegions;
+  std::vector<unsigned char> blk(kBlock, 0);
+  Control ctl{};
+  ctl.epoch = epoch_;
+  ctl.aborted = aborted;
+  std::strncpy(ctl.reason, reason.c_str(), sizeof(ctl.reason) - 1);
+  std::memcpy(blk.data(), &ctl, sizeof(ctl));
   std::vector<Entry> table(kMaxRegions);
   std::memset(table.data(), 0, sizeof(Entry) * kMaxRegions);
   int i = 0;
@@ -374,14 +437,32 @@ void ProcWorld::barrier(size_t rank, Runner& r) {
       DeviceGuard g(b.dev);
       cudaIpcMemHandle_t h;
       KNNG_CUDA(cudaIpcGetMemHandle(&h, b.p));
+      mark_exported(b.p);
       std::memcpy(e.handle, &h, sizeof(h));
     }
   }
-  std::vector<Entry> all(kMaxRegions * num_ranks_);
-  allgather(table.data(), sizeof(Entry) * kMaxRegions, all.data());
-  for (size_t t = 0; t < num_ranks_; ++t)
-    remote_[t].assign(all.begin() + (std::ptrdiff_t)(t * kMaxRegions),
-                      all.begin() + (std::ptrdiff_t)((t + 1) * kMaxRegions));
+  std::memcpy(blk.data() + sizeof(Control), table.data(), sizeof(Entry) * kMaxRegions);
+  std::vector<unsigned char> all(kBlock * num_ranks_);
+  allgather(blk.data(), kBlock, all.data());
+  if (aborted) return;  // the abort notice is out; nothing more to learn
+  for (size_t t = 0; t < num_ranks_; ++t) {
+    Control pc;
+    std::memcpy(&pc, all.data() + t * kBlock, sizeof(pc));
+    if (pc.aborted) {
+      aborted_ = transport_dead_ = true;
+      pc.reason[sizeof(pc.reason) - 1] = 0;
+      throw WorldAborted("world aborted: rank " + std::to_string(t) + ": " + pc.reason);
+    }
+    if (pc.epoch != epoch_) {
+      aborted_ = transport_dead_ = true;
+      throw WorldError("barrier: rank " + std::to_string(t) + " is at epoch " +
+                       std::to_string(pc.epoch) + ", rank " + std::to_string(rank_) + " at " +
+                       std::to_string(epoch_) + " (mismatched barrier counts)");
+    }
+    remote_[t].resize(kMaxRegions);
+    std::memcpy(remote_[t].data(), all.data() + t * kBlock + sizeof(Control),
+                sizeof(Entry) * kMaxRegions);
+  }
 }
 
 uint64_t ProcWorld::get(size_t src, size_t target, const std::string& name, void* dst,
@@ -414,7 +495,19 @@ uint64_t ProcWorld::get(size_t src, size_t target, const std::string& name, void
   return e->bytes;
 }
 
-void ProcWorld::abort(const std::string&) { aborted_ = true; }
+// RankWorld::abort: mark the world failed and tell the peers through one more
+// exchange (their pending barrier all-gather receives it).  No-op once the
+// world already failed or learned of a peer's abort.
+void ProcWorld::abort(const std::string& reason) {
+  if (aborted_) return;
+  aborted_ = true;
+  if (transport_dead_) return;
+  try {
+    exchange_tables(1, reason);
+  } catch (...) {
+  }
+  transport_dead_ = true;
+}
 
 std::vector<GetRecord> ProcWorld::gather_comm_log() {
   struct Rec {

@@ -58,7 +58,8 @@ class World {
 // All ranks are host threads of this process (run_ranks, distsim.hpp:113-198).
 class ThreadWorld : public World {
  public:
-  ThreadWorld(size_t num_ranks, std::chrono::milliseconds watchdog = std::chrono::seconds(600));
+  ThreadWorld(size_t num_ranks, std::chrono::milliseconds watchdog = std::chrono::seconds(600),
+              uint64_t epoch0 = 0);
   ~ThreadWorld() override;
 
   size_t num_ranks() const override { return num_ranks_; }
@@ -112,6 +113,10 @@ class ThreadWorld : public World {
 // NVLink.  A region becomes visible to other ranks at the next barrier -- the
 // refine phase only reads regions after the barrier that follows their
 // publish, so this matches RankWorld for the reference's schedule.
+// Failure handling as RankWorld's (distsim.cpp:84-104): every exchange runs
+// under a watchdog (KNNG_WORLD_WATCHDOG_S, default 600 s) -> WorldError, and a
+// rank that fails aborts the world through its next exchange -> WorldAborted
+// in every peer.
 struct HostTransport {
   void* user = nullptr;
   // out = num_ranks consecutive blocks of `bytes`, in rank order; 0 = success
@@ -135,6 +140,15 @@ class ProcWorld : public World {
   std::vector<GetRecord> gather_comm_log();
 
   static constexpr int kMaxRegions = 8;
+  // per-rank control word of every barrier exchange: an aborting rank's last
+  // collective carries aborted = 1 and its reason, so peers waiting in that
+  // barrier throw WorldAborted (distsim.cpp:96-104); epochs must agree
+  // (mismatched barrier counts are a WorldError, the watchdog's case)
+  struct Control {
+    uint64_t epoch;
+    int32_t aborted, pad;
+    char reason[112];
+  };
   struct Entry {  // fixed-size record exchanged at barriers
     char name[24];
     unsigned char handle[64];  // cudaIpcMemHandle_t
@@ -154,14 +168,17 @@ class ProcWorld : public World {
     uint64_t last_epoch = ~0ull;
   };
   void allgather(const void* in, uint64_t bytes, void* out);
+  void exchange_tables(int aborted, const std::string& reason);
 
   const size_t num_ranks_, rank_;
+  std::chrono::milliseconds watchdog_;
   HostTransport t_;
   std::map<std::string, Slot> mine_;
   std::vector<std::vector<Entry>> remote_;  // [rank][region]
   std::vector<GetRecord> log_;
   uint64_t epoch_ = 0;
   bool aborted_ = false;
+  bool transport_dead_ = false;  // a collective failed or timed out: no more exchanges
 };
 
 }  // namespace knng_b200

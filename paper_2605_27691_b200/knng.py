@@ -146,6 +146,9 @@ _SIGS = {
     "knng_ann_search": (C.c_int, [_vp, C.c_int, C.POINTER(_Dataset), _vp, _u64, _u64,
                                   C.POINTER(_Dataset), C.POINTER(_SearchParams), C.c_uint8, _vp,
                                   _vp, _vp, _vp]),
+    "knng_ann_search_scored_ids": (C.c_int, [_vp, C.c_int, C.POINTER(_Dataset), _vp, _u64, _u64,
+                                             C.POINTER(_Dataset), C.POINTER(_SearchParams),
+                                             C.c_uint8, _vp, _vp, _vp, _vp, _vp, _u64]),
     "knng_partition": (C.c_int, [_vp, C.c_int, C.POINTER(_Dataset), _u64, _u64, C.c_uint8, _vp,
                                  _vp, _vp]),
     "knng_tree_levels": (C.c_int, [_u64, _u64, C.POINTER(_u64)]),
@@ -167,6 +170,10 @@ _SIGS = {
                                                C.POINTER(_SearchParams), _vp]),
     "knng_refine": (C.c_int, [_vp, _vp, _u64, _u64, C.POINTER(_RefineConfig), _vp, _vp, _vp,
                               C.c_int, C.POINTER(_DistResult)]),
+    "knng_refine_phase": (C.c_int, [_vp, _vp, _u64, _u64, C.POINTER(_RefineConfig), _vp, C.c_int,
+                                    C.POINTER(_u64), _vp, _vp, _vp, _vp,
+                                    C.POINTER(_DistResult)]),
+    "knng_effective_groups": (C.c_int, [C.POINTER(_RefineConfig), _vp, _u64, C.POINTER(_u64)]),
     "knng_last_comm_log": (C.c_int, [_vp, _vp, _u64, C.POINTER(_u64)]),
     "knng_brute_force": (C.c_int, [_vp, C.c_int, C.POINTER(_Dataset), _vp, _u64, _u64, C.c_uint8,
                                    _vp, _vp]),
@@ -950,6 +957,55 @@ def refine(x_perm, cfg: RefineConfig, offsets, ids, dists, mode: int = 0) -> Dis
     _check(lib().knng_refine(context().h, _ptr(x), x.shape[0], x.shape[1], C.byref(cc),
                              _ptr(off), _ptr(ids), _ptr(dists), mode, C.byref(res)))
     return _dist_result(KnnGraph(ids, dists), res)
+
+
+def effective_groups(cfg: RefineConfig, offsets, dims: int) -> int:
+    """refine.cpp:160-183: M, or P when the tree phase is skipped."""
+    off = np.ascontiguousarray(offsets, np.uint64)
+    cc = cfg._c()
+    cc.ranks = len(off) - 1
+    out = _u64(0)
+    _check(lib().knng_effective_groups(C.byref(cc), _ptr(off), dims, C.byref(out)))
+    return out.value
+
+
+REFINE_PHASES = {"all_to_all_refine": 1, "binary_tree_refine": 2, "grouped_merge": 3,
+                 "flat_refine": 4}
+
+
+def refine_phase(x_perm, cfg: RefineConfig, offsets, ids, dists, phase: str, epoch: int = 0,
+                 group_graphs=None):
+    """One world-level phase driver (refine.hpp:117-136) on a world at `epoch`.
+    Returns (graph, group search graphs (grouped_merge) or None, epoch after,
+    DistBuildResult with the phase's gets).  group_graphs (flat_refine): the
+    per-rank blocks grouped_merge returned."""
+    x = np.ascontiguousarray(x_perm, np.float32)
+    ids = np.array(ids, np.uint32, copy=True)
+    dists = np.array(dists, np.float32, copy=True)
+    off = np.ascontiguousarray(offsets, np.uint64)
+    cc = cfg._c()
+    cc.ranks = len(off) - 1
+    ph = REFINE_PHASES[phase]
+    od = cfg.out_degree or cfg.k
+    g = effective_groups(cfg, off, x.shape[1])
+    gsz = (len(off) - 1) // g
+    blocks = [int(off[(r // gsz) * gsz + gsz] - off[(r // gsz) * gsz]) * od
+              for r in range(len(off) - 1)]
+    sg_out = np.zeros(sum(blocks), np.uint32) if ph == 3 else None
+    sg_in = (np.ascontiguousarray(np.concatenate([np.asarray(b, np.uint32).ravel()
+                                                  for b in group_graphs]))
+             if ph == 4 else None)
+    ep = _u64(epoch)
+    res = _DistResult()
+    _check(lib().knng_refine_phase(context().h, _ptr(x), x.shape[0], x.shape[1], C.byref(cc),
+                                   _ptr(off), ph, C.byref(ep), _ptr(ids), _ptr(dists),
+                                   _ptr(sg_in) if sg_in is not None else None,
+                                   _ptr(sg_out) if sg_out is not None else None, C.byref(res)))
+    sgs = None
+    if sg_out is not None:
+        at = np.cumsum([0] + blocks)
+        sgs = [sg_out[at[r]:at[r + 1]].reshape(-1, od) for r in range(len(blocks))]
+    return KnnGraph(ids, dists), sgs, ep.value, _dist_result(KnnGraph(ids, dists), res)
 
 
 def brute_force_knng(x, k: int, rows=None, device: Optional[int] = None, metric: str = "l2"):

@@ -72,3 +72,66 @@ def test_rank_processes_match_single_process(knng, tmp_path, world, metric):
         want = sorted((g.src, g.target, g.bytes, g.epoch) for g in ref.comm_log)
         assert got == want
     assert seen.all()
+
+
+def _fail_main(rank, world, port, out_dir, mode):
+    """mode 'abort': rank 1 fails after its local build (KNNG_INJECT_FAIL_RANK);
+    mode 'absent': rank 1 never joins the build (the others' watchdog fires)."""
+    import json
+    import time
+
+    import torch
+    import torch.distributed as dist
+    import paper_2605_27691_b200 as knng
+    os.environ["KNNG_WORLD_WATCHDOG_S"] = "20"
+    if mode == "abort":
+        os.environ["KNNG_INJECT_FAIL_RANK"] = "1"
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    dev = rank % torch.cuda.device_count()
+    x = torch.from_numpy(knng.gen_random_dataset(8000, 16, "clustered", 42, 16)).to(f"cuda:{dev}")
+    cfg = knng.RefineConfig(ranks=world, groups=2, k=16, seed=7,
+                            nn=knng.NnDescentParams(k=16, seed=3),
+                            search=knng.SearchParams(k_s=16, beam_width=64, seed=5))
+    t = time.time()
+    outcome = "ok"
+    if mode == "absent" and rank == 1:
+        outcome = "absent"
+        time.sleep(45)
+    else:
+        try:
+            knng.build_distributed_rank(x, cfg, rank, world)
+        except knng.WorldAborted as e:
+            outcome = "WorldAborted: " + str(e)
+        except knng.WorldError as e:
+            outcome = "WorldError: " + str(e)
+        except Exception as e:  # noqa: BLE001
+            outcome = type(e).__name__ + ": " + str(e)
+    with open(os.path.join(out_dir, f"r{rank}.json"), "w") as f:
+        json.dump({"outcome": outcome, "secs": time.time() - t}, f)
+    os._exit(0)  # a rank may have a transport thread still blocked in gloo
+
+
+@pytest.mark.parametrize("world,mode", [(2, "abort"), (4, "abort"), (2, "absent")])
+def test_rank_failure_propagates(knng, tmp_path, world, mode):
+    """distsim.cpp:84-104 / test_distsim.cpp:48-57, 177-185 for one process
+    per GPU: a failing rank aborts the world (its peers raise WorldAborted
+    naming it, promptly), and a rank that never arrives trips the watchdog
+    (WorldError) instead of hanging its peers."""
+    import json
+
+    import torch.multiprocessing as mp
+    ctx = mp.start_processes(_fail_main, args=(world, _free_port(), str(tmp_path), mode),
+                             nprocs=world, join=False, start_method="spawn")
+    ctx.join(timeout=240)
+    res = [json.load(open(tmp_path / f"r{r}.json")) for r in range(world)]
+    if mode == "abort":
+        assert "injected failure at rank 1" in res[1]["outcome"], res
+        for r in range(world):
+            if r != 1:
+                assert res[r]["outcome"].startswith("WorldAborted"), res
+                assert "rank 1" in res[r]["outcome"], res
+                assert res[r]["secs"] < 60, res
+    else:
+        assert res[0]["outcome"].startswith("WorldError") and "watchdog" in res[0]["outcome"], res
+        assert 15 < res[0]["secs"] < 60, res

@@ -185,3 +185,31 @@ def test_cosine_stages(golden, oracle):
     assert np.array_equal(h, g["s_hops"]) and np.array_equal(s, g["s_scored"])
     bi, bd = oracle.brute_force_rows(x, np.arange(len(x)), 10, metric=1)
     assert np.array_equal(bi, g["bf_ids"]) and np.array_equal(bits(bd), bits(g["bf_d"]))
+
+
+MEMORY_CASES = {  # tests/golden/make_golden_memory.py (double_buffer is timing-only)
+    "p4_skip": (4, 2, True, 0, 64, 16), "p4_concat1": (4, 2, False, 1, 64, 16),
+    "p4_concat1g": (4, 2, False, 1 << 30, 64, 16), "p8_skip": (8, 2, True, 0, 128, 96),
+    "p8_concat1": (8, 2, False, 1, 128, 96), "p8_m4": (8, 4, False, 0, 64, 16),
+    "p8_m4_db": (8, 4, False, 0, 64, 16)}
+
+
+@pytest.mark.parametrize("name", sorted(MEMORY_CASES))
+def test_memory_pressure_paths_vs_reference(golden, oracle, name):
+    """skip_tree_phase / max_concat_bytes (refine.cpp:160-183) and M = 4 with
+    double_buffer (refine.cpp:343-350): the C restatement equals the unmodified
+    reference on the same local graphs."""
+    g, m = golden("distributed"), golden("memory_paths")
+    P, M, skip, mcb, beam, ent = MEMORY_CASES[name]
+    cfg = oracle.refine_config(P, M, 16, nn_seed=2, search_seed=2, seed=2, beam_width=beam,
+                               num_entry_points=ent, skip_tree=skip, max_concat_bytes=mcb)
+    te, off = oracle.partition(2000, P, 2)
+    i, d = oracle.refine_from_local(g["x"], cfg, te, off, g[f"local{P}_ids"],
+                                    g[f"local{P}_d"], 0)
+    assert np.array_equal(i, m[name + "_ids"]) and np.array_equal(bits(d), bits(m[name + "_d"]))
+    if name in ("p4_skip", "p4_concat1", "p8_skip", "p8_concat1"):
+        # the skip really changed the schedule (else the case would not test it)
+        base = g["refine4_ids"] if P == 4 else g["refine8_ids"]
+        assert not np.array_equal(i, base)
+    if name == "p4_concat1g":
+        assert np.array_equal(i, g["refine4_ids"])

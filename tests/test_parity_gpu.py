@@ -465,3 +465,61 @@ def test_cpp_dropin_reference_cases(knng):
                          text=True, timeout=600)
     print(res.stdout)
     assert res.returncode == 0, res.stdout + res.stderr
+
+
+# ---------------------------------------------------------------------------
+# memory-pressure paths (refine.cpp:160-183, 343-350) and the standalone
+# world-level phase drivers (refine.hpp:117-136), bit-exact vs the reference
+# ---------------------------------------------------------------------------
+
+MEMORY_CASES = {  # tests/golden/make_golden_memory.py
+    "p4_skip": (4, 2, True, 0, False, 64, 16), "p4_concat1": (4, 2, False, 1, False, 64, 16),
+    "p4_concat1g": (4, 2, False, 1 << 30, False, 64, 16),
+    "p8_skip": (8, 2, True, 0, False, 128, 96), "p8_concat1": (8, 2, False, 1, False, 128, 96),
+    "p8_m4": (8, 4, False, 0, False, 64, 16), "p8_m4_db": (8, 4, False, 0, True, 64, 16)}
+
+
+@pytest.mark.parametrize("name", sorted(MEMORY_CASES))
+def test_memory_pressure_paths_bitexact(knng, golden, name):
+    g, m = golden("distributed"), golden("memory_paths")
+    P, M, skip, mcb, db, beam, ent = MEMORY_CASES[name]
+    cfg = knng.RefineConfig(ranks=P, groups=M, k=16, seed=2, skip_tree_phase=skip,
+                            max_concat_bytes=mcb, double_buffer=db,
+                            nn=knng.NnDescentParams(k=16, seed=2),
+                            search=knng.SearchParams(k_s=16, beam_width=beam,
+                                                     num_entry_points=ent, seed=2))
+    r = knng.refine(g[f"x_perm{P}"], cfg, g[f"off{P}"], g[f"local{P}_ids"], g[f"local{P}_d"],
+                    mode=0)
+    assert np.array_equal(r.graph.ids, m[name + "_ids"])
+    assert np.array_equal(bits(r.graph.dists), bits(m[name + "_d"]))
+    levels = 0 if (skip or mcb == 1) else knng.tree_levels(P, M)
+    assert r.levels == levels
+
+
+def test_phase_drivers_chain_equals_pipeline(knng, golden):
+    """binary_tree_refine -> grouped_merge -> flat_refine, one call each on one
+    world (epochs carried between the calls), equals the composed refine, and
+    every member of a group holds the identical group search graph
+    (test_refine.cpp:244-259)."""
+    g = golden("distributed")
+    cfg = knng.RefineConfig(ranks=4, groups=2, k=16, seed=2,
+                            nn=knng.NnDescentParams(k=16, seed=2),
+                            search=knng.SearchParams(k_s=16, beam_width=64, seed=2))
+    x, off = g["x_perm4"], g["off4"]
+    g1, _, ep, r1 = knng.refine_phase(x, cfg, off, g["local4_ids"], g["local4_d"],
+                                      "binary_tree_refine")
+    assert ep == 1 + knng.tree_levels(4, 2)
+    _, sgs, ep, r2 = knng.refine_phase(x, cfg, off, g1.ids, g1.dists, "grouped_merge", ep)
+    assert np.array_equal(sgs[0], sgs[1]) and np.array_equal(sgs[2], sgs[3])
+    assert sgs[0].shape[0] == int(off[2] - off[0])
+    g3, _, ep, r3 = knng.refine_phase(x, cfg, off, g1.ids, g1.dists, "flat_refine", ep, sgs)
+    assert np.array_equal(g3.ids, g["refine4_ids"])
+    assert np.array_equal(bits(g3.dists), bits(g["refine4_d"]))
+    # flat pulls hit the other group's datasets, at the world's epoch after the setup barrier
+    for rk in range(4):
+        tg = {c.target for c in r3.comm_log if c.src == rk and c.region == "dataset"}
+        assert tg == ({2, 3} if rk < 2 else {0, 1})
+        assert all(c.epoch == ep for c in r3.comm_log)
+    ga, _, _, _ = knng.refine_phase(x, cfg, off, g["local4_ids"], g["local4_d"],
+                                    "all_to_all_refine")
+    assert np.array_equal(ga.ids, g["a2a4_ids"])
