@@ -151,6 +151,7 @@ void stage_rows(Runner& r, const knng_dataset* ds, DevData& out, int slot);
 void stage(Runner& r, const knng_dataset* ds, DevData& out, int slot = 0) {
   stage_rows(r, ds, out, slot);
   if (ds->metric == KNNG_METRIC_COS) {
+    DeviceGuard g(r.device);
     out.nrm_own.alloc(r, ds->n ? ds->n : 1);
     row_norms_device(r, out.p, ds->n, (int)ds->dims, out.nrm_own.p);
     out.nrm = out.nrm_own.p;
@@ -161,6 +162,7 @@ void stage(Runner& r, const knng_dataset* ds, DevData& out, int slot = 0) {
 // re-allocate hundreds of MB each time.
 void stage_rows(Runner& r, const knng_dataset* ds, DevData& out, int slot) {
   check_ds(ds);
+  DeviceGuard g(r.device);  // the caller's current device may be another GPU
   if (ds->elem_kind == KNNG_ELEM_U8) {
     const u64 cells = ds->n * ds->dims;
     out.own.alloc(r, cells);

@@ -306,6 +306,221 @@ __global__ __launch_bounds__(256) void k_rev_select(u64 n, u32 B, u64 iter_seed,
 }
 
 // ---------------------------------------------------------------------------
+// Reverse lists inside nn_descent without the sort.  Only the SET of a
+// reverse list matters to the join when it is not sampled (the join lists are
+// deduplicated unions, and every pair they produce is offered to
+// order-independent buckets), so sources are scattered straight into their
+// targets' segments with per-target atomic cursors.  A segment longer than
+// the bound is sampled by RANK in ascending source order (the reference's
+// serial transpose order, nndescent.cpp:108-127): k_rev_select_rank ranks it
+// (warp bitonic sort <= 32, rank counting in smem <= kRankSmem, rank counting
+// in global memory beyond), so the picks equal the sorted path's.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void rev_put(u32 t, bool on, u32 p, const u64* __restrict__ off,
+                                        u32* __restrict__ cur, u32* __restrict__ buf) {
+  // lanes of one warp often share a hub target: one atomic per distinct target
+  const unsigned act = __ballot_sync(kFull, on);
+  if (!on) return;
+  const unsigned grp = __match_any_sync(act, t);
+  const int leader = __ffs(grp) - 1;
+  u32 base = 0;
+  if ((int)lane_id() == leader) base = atomicAdd(&cur[t], (u32)__popc(grp));
+  base = __shfl_sync(grp, base, leader);
+  buf[off[t] + base + __popc(grp & lanemask_lt())] = p;
+}
+
+// lane = source (32 consecutive sources per warp), one list slot per round
+__global__ __launch_bounds__(256) void k_rev_scatter(u64 n, u32 k, u32 B, const u32* __restrict__ nf,
+                                                     const u32* __restrict__ nfn,
+                                                     const u32* __restrict__ of,
+                                                     const u32* __restrict__ ofn,
+                                                     const u32* __restrict__ cnt_new,
+                                                     const u64* __restrict__ off_new,
+                                                     const u64* __restrict__ off_old,
+                                                     u32* __restrict__ cur_new,
+                                                     u32* __restrict__ cur_old,
+                                                     u32* __restrict__ buf_new,
+                                                     u32* __restrict__ buf_old) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 p0 = ((((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * 32; p0 < n;
+       p0 += warps * 32) {
+    const u64 p = p0 + lane;
+    const bool live = p < n;
+    const u32 cn = live ? nfn[p] : 0, co = live ? ofn[p] : 0;
+    const u32 mx = __reduce_max_sync(kFull, cn > co ? cn : co);
+    for (u32 j = 0; j < mx; ++j) {
+      const bool on_n = j < cn;
+      const u32 tn = on_n ? nf[p * B + j] : 0;
+      rev_put(tn, on_n, (u32)p, off_new, cur_new, buf_new);
+      bool on_o = j < co;
+      const u32 to = on_o ? of[p * k + j] : 0;
+      on_o = on_o && joins(to, nfn, cnt_new);
+      rev_put(to, on_o, (u32)p, off_old, cur_old, buf_old);
+    }
+  }
+}
+
+constexpr u32 kRankSmem = 512;  // per-warp smem rank sort capacity
+
+__global__ __launch_bounds__(256) void k_rev_select_rank(u64 n, u32 B, u64 iter_seed,
+                                                         const u64* __restrict__ off_new,
+                                                         const u32* __restrict__ buf_new,
+                                                         const u64* __restrict__ off_old,
+                                                         const u32* __restrict__ buf_old,
+                                                         u32* __restrict__ nr,
+                                                         u32* __restrict__ nrn,
+                                                         u32* __restrict__ orv,
+                                                         u32* __restrict__ orn,
+                                                         u32* __restrict__ long_cnt,
+                                                         u32* __restrict__ long_rec) {
+  __shared__ u32 s_pick[8][32];
+  __shared__ u32 s_seg[8][kRankSmem];
+  const unsigned lane = lane_id();
+  const int w = threadIdx.x >> 5;
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 v = (((u64)blockIdx.x * blockDim.x) >> 5) + w; v < n; v += warps) {
+    const u64 rs = mix_seed(iter_seed, 0x8000000000000000ull | v);
+    u64 drawn = 0;  // rng position, shared by new_rev then old_rev
+    u32* sp = s_pick[w];
+    for (int which = 0; which < 2; ++which) {
+      const u64* off = which ? off_old : off_new;
+      const u32* buf = which ? buf_old : buf_new;
+      u32* out = (which ? orv : nr) + v * B;
+      u32* outn = which ? orn : nrn;
+      const u64 lo = off[v];
+      const u32 len = (u32)(off[v + 1] - lo);
+      const u32* seg = buf + lo;
+      if (len <= B) {  // taken whole: its order is irrelevant to the join
+        if (lane < len) out[lane] = seg[lane];
+        if (lane == 0) outn[v] = len;
+        continue;
+      }
+      drawn += warp_sample_distinct(rs, drawn, len, B, sp);
+      if (len <= 32) {
+        // ascending sort across the warp, then pick ranks
+        const u64 x = lane < len ? (u64)seg[lane] : ~0ull;
+        const u32 sorted = (u32)warp_sort32(x);
+        const u32 pick = __shfl_sync(kFull, sorted, lane < B ? sp[lane] : 0);
+        if (lane < B) out[lane] = pick;
+      } else if (len <= kRankSmem) {
+        // bitonic sort of the segment (padded to a power of two) in smem
+        u32* ss = s_seg[w];
+        u32 m = 64;
+        while (m < len) m <<= 1;
+        for (u32 i = lane; i < m; i += 32) ss[i] = i < len ? seg[i] : 0xffffffffu;
+        __syncwarp();
+        for (u32 size = 2; size <= m; size <<= 1)
+          for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
+            for (u32 i = lane; i < m; i += 32) {
+              const u32 partner = i ^ stride;
+              if (partner > i) {
+                const u32 a0 = ss[i], a1 = ss[partner];
+                const bool up = (i & size) == 0;
+                if ((a0 > a1) == up) {
+                  ss[i] = a1;
+                  ss[partner] = a0;
+                }
+              }
+            }
+            __syncwarp();
+          }
+        if (lane < B) out[lane] = ss[sp[lane]];
+        __syncwarp();
+      } else {
+        // long (hub) segment: deferred to k_rev_select_long (radix select)
+        u32 slot = 0;
+        if (lane == 0) slot = atomicAdd(long_cnt, 1u);
+        slot = __shfl_sync(kFull, slot, 0);
+        u32* rec = long_rec + (u64)slot * (2 + 32);
+        if (lane == 0) {
+          rec[0] = (u32)v;
+          rec[1] = (u32)which;
+        }
+        if (lane < B) rec[2 + lane] = sp[lane];
+      }
+      if (lane == 0) outn[v] = B;
+      __syncwarp();
+    }
+  }
+}
+
+// Hub segments (longer than kRankSmem): one CTA each selects the elements of
+// the B sampled ranks by radix select over the segment in global memory --
+// four 8-bit passes; after them each rank's prefix IS its element (sources
+// in a segment are distinct).  O(len) per segment, however long.
+__global__ __launch_bounds__(256) void k_rev_select_long(u64 n_src, u32 B,
+                                                         const u64* __restrict__ off_new,
+                                                         const u32* __restrict__ buf_new,
+                                                         const u64* __restrict__ off_old,
+                                                         const u32* __restrict__ buf_old,
+                                                         u32* __restrict__ nr,
+                                                         u32* __restrict__ orv,
+                                                         const u32* __restrict__ long_cnt,
+                                                         const u32* __restrict__ long_rec) {
+  __shared__ u32 hist[32][256];
+  __shared__ u32 prefix[32], remain[32], lead[32];
+  const u32 nrec = *long_cnt;
+  // source ids are < n: digits start at the top bits that vary (a first digit
+  // of all-zero high bits would pile every element onto one histogram bin)
+  int top = 0;
+  while (top < 32 && (n_src >> top) > 0) ++top;
+  const int first_shift = top > 8 ? ((top - 8 + 7) / 8) * 8 : 0;
+  for (u32 e = blockIdx.x; e < nrec; e += gridDim.x) {
+    const u32* rec = long_rec + (u64)e * (2 + 32);
+    const u64 v = rec[0];
+    const int which = (int)rec[1];
+    const u64* off = which ? off_old : off_new;
+    const u32* seg = (which ? buf_old : buf_new) + off[v];
+    const u32 len = (u32)(off[v + 1] - off[v]);
+    if (threadIdx.x < B) {
+      prefix[threadIdx.x] = 0;
+      remain[threadIdx.x] = rec[2 + threadIdx.x];
+    }
+    for (int shift = first_shift; shift >= 0; shift -= 8) {
+      for (u32 i = threadIdx.x; i < B * 256; i += blockDim.x) hist[i >> 8][i & 255] = 0;
+      __syncthreads();
+      const u32 hi_mask = shift >= 24 ? 0u : (0xffffffffu << (shift + 8));
+      // ranks sharing the bits decided so far share one histogram (its leader)
+      if (threadIdx.x < B) {
+        u32 l = threadIdx.x;
+        for (u32 b = 0; b < threadIdx.x; ++b)
+          if ((prefix[b] & hi_mask) == (prefix[threadIdx.x] & hi_mask)) {
+            l = b;
+            break;
+          }
+        lead[threadIdx.x] = l;
+      }
+      __syncthreads();
+      for (u32 i = threadIdx.x; i < len; i += blockDim.x) {
+        const u32 x = seg[i];
+        for (u32 b = 0; b < B; ++b)
+          if (lead[b] == b && (x & hi_mask) == (prefix[b] & hi_mask)) {
+            atomicAdd(&hist[b][(x >> shift) & 255], 1u);
+            break;  // the groups' prefixes are disjoint
+          }
+      }
+      __syncthreads();
+      if (threadIdx.x < B) {
+        const u32 b = threadIdx.x;
+        const u32 hb = lead[b];
+        u32 acc = 0, bin = 0;
+        for (; bin < 256; ++bin) {
+          const u32 h = hist[hb][bin];
+          if (acc + h > remain[b]) break;
+          acc += h;
+        }
+        prefix[b] |= bin << shift;
+        remain[b] -= acc;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x < B) (which ? orv : nr)[v * B + threadIdx.x] = prefix[threadIdx.x];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // apply_candidates nndescent.cpp:199-223 -- warp per point
 // ---------------------------------------------------------------------------
 // With X set the buckets hold LOWER BOUNDS of the exact distances (the
@@ -464,11 +679,19 @@ void init_random_graph_device(Runner& r, const DevRows& ds, uint32_t k, uint64_t
 
 namespace {
 
-struct RevCsr {
-  DBuf<u32> cnt_new, cnt_old, src_cnt;
-  DBuf<u64> off_new, off_old, src_off_new, src_off_old;
-  DBuf<u32> key_new, val_new, key_old, val_old, tk_new, tv_new, tk_old, tv_old;
-};
+
+// Which reverse-list path nn_descent takes (both give bit-identical graphs,
+// tests/test_parity_gpu.py).  The scatter path is random-access bound: it wins
+// while its per-target cursor/offset arrays stay L2-resident (C2 1M points:
+// sampling 24.9 -> 21.6 ms per build) and loses to the radix sort's streaming
+// passes beyond (C4 10M points: 2.24 -> 2.65 s; profiles/r02_sampling_paths.md),
+// so it is used up to 2M points.  KNNG_REV_SORT=1 / =0 forces either path.
+bool rev_sort_forced(uint64_t n) {
+  const char* v = std::getenv("KNNG_REV_SORT");
+  if (v && v[0] == '1') return true;
+  if (v && v[0] == '0') return false;
+  return n > (2ull << 20);
+}
 
 void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_seed,
                  const uint64_t* keys, uint32_t* flags, SampleLists& s, RevCsr& c, bool prune_old,
@@ -498,6 +721,28 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
     exclusive_scan_u32(r, s.ofn.p, c.src_off_old.p, n);
   }
   lap("old_count+scan");
+  if (prune_old && !rev_sort_forced(n)) {
+    // inside nn_descent: scatter + rank-sampled reverse lists (no sort)
+    exclusive_scan_u32(r, c.cnt_new.p, c.off_new.p, n);
+    exclusive_scan_u32(r, c.cnt_old.p, c.off_old.p, n);
+    c.cur_new.zero();
+    c.cur_old.zero();
+    k_rev_scatter<<<g, 256, 0, r.stream>>>(n, k, B, s.nf.p, s.nfn.p, s.of.p, s.ofn.p,
+                                           c.cnt_new.p, c.off_new.p, c.off_old.p, c.cur_new.p,
+                                           c.cur_old.p, c.key_new.p, c.key_old.p);
+    KNNG_LAUNCH_CHECK();
+    c.long_cnt.zero();
+    k_rev_select_rank<<<g, 256, 0, r.stream>>>(n, B, iter_seed, c.off_new.p, c.key_new.p,
+                                               c.off_old.p, c.key_old.p, s.nr.p, s.nrn.p,
+                                               s.orv.p, s.orn.p, c.long_cnt.p, c.long_rec.p);
+    KNNG_LAUNCH_CHECK();
+    k_rev_select_long<<<r.num_sms * 2, 256, 0, r.stream>>>(n, B, c.off_new.p, c.key_new.p,
+                                                           c.off_old.p, c.key_old.p, s.nr.p,
+                                                           s.orv.p, c.long_cnt.p, c.long_rec.p);
+    KNNG_LAUNCH_CHECK();
+    if (launches) *launches += 4 + 2 + 2 * 3 + 3;
+    return;
+  }
   exclusive_scan_u32(r, s.nfn.p, c.src_off_new.p, n);
   exclusive_scan_u32(r, c.cnt_new.p, c.off_new.p, n);
   exclusive_scan_u32(r, c.cnt_old.p, c.off_old.p, n);
@@ -539,6 +784,11 @@ void alloc_lists(Runner& r, uint64_t n, uint32_t k, uint32_t B, SampleLists& s, 
   s.orn.alloc(r, n);
   c.cnt_new.alloc(r, n);
   c.cnt_old.alloc(r, n);
+  c.cur_new.alloc(r, n);
+  c.cur_old.alloc(r, n);
+  // hub segments (> kRankSmem entries): at most (new + old entries) / kRankSmem
+  c.long_cnt.alloc(r, 1);
+  c.long_rec.alloc(r, (n * (b + k) / kRankSmem + 2) * (2 + 32));
   c.off_new.alloc(r, n + 1);
   c.off_old.alloc(r, n + 1);
   c.src_cnt.alloc(r, n);
@@ -593,25 +843,36 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   StageTimer tm(time_kernels, r.stream);
   const auto t_call = std::chrono::steady_clock::now();
 
-  DBuf<float> worst(r, n);
-  DBuf<u64> slots_own;
-  u64* slots_p = ws_buf(r, ws ? &ws->slots : nullptr, slots_own, n * S);
+  // per-build buffers: the context's workspace (grow-only, reused across
+  // builds on this device), else owned by this call
+  NndWorkspace own_ws;
+  NndWorkspace& W = ws ? *ws : own_ws;
+  float* worst_p = ws_buf(r, &W.worst, W.worst, n);
+  u64* slots_p = ws_buf(r, &W.slots, W.slots, n * S);
   KNNG_CUDA(cudaMemsetAsync(slots_p, 0xff, n * S * sizeof(u64), r.stream));
-  DBuf<u64> counters(r, kNumCounters);
+  u64* counters_p = ws_buf(r, &W.counters, W.counters, kNumCounters);
+  auto zero_counters = [&] {
+    KNNG_CUDA(cudaMemsetAsync(counters_p, 0, kNumCounters * sizeof(u64), r.stream));
+  };
   HBuf<u64> hcount(kNumCounters);
-  SampleLists s;
-  RevCsr c;
-  alloc_lists(r, n, k, B, s, c);
+  if (W.lists_n < n || W.lists_k != k || W.lists_b != B) {
+    alloc_lists(r, n, k, B, W.lists, W.rev);
+    W.lists_n = n;
+    W.lists_k = k;
+    W.lists_b = B;
+  }
+  SampleLists& s = W.lists;
+  RevCsr& c = W.rev;
   uint64_t launches = 0;
 
-  launch_init(r, ds, k, p.seed, keys, flags, worst.p);
+  launch_init(r, ds, k, p.seed, keys, flags, worst_p);
   ++launches;
   tm.tick(kStInit);
 
   // join lists (compact per point) + join launch shape
   const JoinPlan plan = plan_join(r, ds.d, k, B);
-  DBuf<u32> L_ids_own, L_cnt(r, n);
-  u32* L_ids_p = ws_buf(r, ws ? &ws->L_ids : nullptr, L_ids_own, n * plan.RMAX);
+  u32* L_cnt_p = ws_buf(r, &W.L_cnt, W.L_cnt, n);
+  u32* L_ids_p = ws_buf(r, &W.L_ids, W.L_ids, n * plan.RMAX);
   // Offer queue: each point chunk owns a region sized for its worst case (2
   // offers per pair, max pairs C(2B,2) + 2B(k+B)), so nothing can overflow;
   // points are processed in slices to bound the queue (budget below).
@@ -619,52 +880,58 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   // what the pool holds unused from earlier calls (cudaMemGetInfo counts that
   // as used, so the budget -- and the queue size -- drifted between builds
   // and a later build had to map tens of GB afresh)
-  size_t free_b = 0, total_b = 0;
-  KNNG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  {
-    cudaMemPool_t pool;
-    uint64_t reserved = 0, used = 0;
-    if (cudaDeviceGetDefaultMemPool(&pool, r.device) == cudaSuccess &&
-        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) ==
-            cudaSuccess &&
-        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
-        reserved > used)
-      free_b += reserved - used;
-    cudaGetLastError();
+  // the slicing is decided once per (n, queue-region) shape and kept in the
+  // workspace: a warm build makes no memory query
+  u64 chunks_per_slice = W.q_chunks_per_slice;
+  if (!(W.q_n == n && W.q_per_chunk == plan.q_per_chunk && chunks_per_slice)) {
+    size_t free_b = 0, total_b = 0;
+    KNNG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    {
+      cudaMemPool_t pool;
+      uint64_t reserved = 0, used = 0;
+      if (cudaDeviceGetDefaultMemPool(&pool, r.device) == cudaSuccess &&
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) ==
+              cudaSuccess &&
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+          reserved > used)
+        free_b += reserved - used;
+      cudaGetLastError();
+    }
+    free_b += W.q_key.n * 8 + W.q_tgt.n * 4;  // reused below
+    // up to 64 GB of worst-case queue (B200: 180 GB HBM): C2 runs as a single
+    // slice (one join + one offer launch per iteration)
+    const u64 budget = std::min<u64>(64ull << 30, free_b / 3);
+    chunks_per_slice = std::max<u64>(1, budget / (plan.q_per_chunk * 12));
+    chunks_per_slice = std::min<u64>(chunks_per_slice, ceil_div<u64>(n, (u64)kJoinChunk));
+    W.q_chunks_per_slice = chunks_per_slice;
+    W.q_per_chunk = plan.q_per_chunk;
+    W.q_n = n;
   }
-  if (ws) free_b += ws->q_key.n * 8 + ws->q_tgt.n * 4;  // reused below
-  // up to 64 GB of worst-case queue (B200: 180 GB HBM): C2 runs as a single
-  // slice (one join + one offer launch per iteration)
-  const u64 budget = std::min<u64>(64ull << 30, free_b / 3);
-  u64 chunks_per_slice = std::max<u64>(1, budget / (plan.q_per_chunk * 12));
   u64 slice = chunks_per_slice * kJoinChunk;
-  if (slice > n) {
-    slice = n;
-    chunks_per_slice = ceil_div<u64>(n, (u64)kJoinChunk);
-  }
-  DBuf<u64> q_key_own;
-  DBuf<u32> q_tgt_own, q_fill(r, chunks_per_slice);
-  u64* q_key_p = ws_buf(r, ws ? &ws->q_key : nullptr, q_key_own, chunks_per_slice * plan.q_per_chunk);
-  u32* q_tgt_p = ws_buf(r, ws ? &ws->q_tgt : nullptr, q_tgt_own, chunks_per_slice * plan.q_per_chunk);
-  DBuf<u32> chunk_ctr(r, 1);
+  if (slice > n) slice = n;
+  u32* q_fill_p = ws_buf(r, &W.q_fill, W.q_fill, chunks_per_slice);
+  u64* q_key_p = ws_buf(r, &W.q_key, W.q_key, chunks_per_slice * plan.q_per_chunk);
+  u32* q_tgt_p = ws_buf(r, &W.q_tgt, W.q_tgt, chunks_per_slice * plan.q_per_chunk);
+  u32* chunk_ctr_p = ws_buf(r, &W.chunk_ctr, W.chunk_ctr, 1);
   // points with a new entry, compacted: late iterations join a small fraction
-  DBuf<u32> act(r, n), act_flag(r, n);
-  DBuf<u64> act_off(r, n + 1);
+  u32* act_p = ws_buf(r, &W.act, W.act, n);
+  u32* act_flag_p = ws_buf(r, &W.act_flag, W.act_flag, n);
+  u64* act_off_p = ws_buf(r, &W.act_off, W.act_off, n + 1);
   JoinLaunch jl;
-  jl.act = act.p;
+  jl.act = act_p;
   jl.X = ds.x;
   jl.nrm = ds.nrm;
   jl.d = ds.d;
   jl.n_rows = n;
   const bool use_tc = join_tc_supported(ds.x, ds.d, k, B, ds.nrm != nullptr);
   jl.L_ids = L_ids_p;
-  jl.L_cnt = L_cnt.p;
-  jl.worst = worst.p;
-  jl.chunk_counter = chunk_ctr.p;
+  jl.L_cnt = L_cnt_p;
+  jl.worst = worst_p;
+  jl.chunk_counter = chunk_ctr_p;
   jl.q_key = q_key_p;
   jl.q_tgt = q_tgt_p;
-  jl.q_fill = q_fill.p;
-  jl.counters = counters.p;
+  jl.q_fill = q_fill_p;
+  jl.counters = counters_p;
 
   if (st) *st = NndStats{};
   const double threshold = p.delta * (double)k * (double)n;
@@ -675,45 +942,45 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
     ~EvGuard() { cudaEventDestroy(e); }
   } iter_done_guard{iter_done};
   for (u64 iter = 0; iter < p.max_iters; ++iter) {
-    counters.zero();
+    zero_counters();
     const u64 iter_seed = mix_seed(p.seed, 0x5a3f1e00ull + iter);
     sample_into(r, n, k, B, iter_seed, keys, flags, s, c, true, &launches);
     tm.tick(kStSample);
     launch_join_lists(r, n, k, B, plan.RMAX, s.nf.p, s.nfn.p, s.of.p, s.ofn.p, s.nr.p, s.nrn.p,
-                      s.orv.p, s.orn.p, L_ids_p, L_cnt.p);
+                      s.orv.p, s.orn.p, L_ids_p, L_cnt_p);
     ++launches;
     tm.tick(kStLists);
-    build_active_list(r, n, L_cnt.p, act_flag.p, act_off.p, act.p);
+    build_active_list(r, n, L_cnt_p, act_flag_p, act_off_p, act_p);
     launches += 5;
     // the active count stays on the device: every slice is launched and its
     // kernels bound themselves by it (no host round trip mid-iteration; the
     // slices past the count exit at once)
-    jl.n_live = act_off.p + n;
+    jl.n_live = act_off_p + n;
     const u64 nslices = ceil_div<u64>(n, slice);
     for (u64 si = 0; si < nslices; ++si) {
       jl.p_lo = si * slice;
       jl.p_hi = std::min<u64>(n, jl.p_lo + slice);
-      chunk_ctr.zero();
+      KNNG_CUDA(cudaMemsetAsync(chunk_ctr_p, 0, sizeof(u32), r.stream));
       tm.tick(kStLists);
       if (use_tc) {
-        q_fill.zero();
+        KNNG_CUDA(cudaMemsetAsync(q_fill_p, 0, chunks_per_slice * sizeof(u32), r.stream));
         launch_join_tc(r, plan, jl);
       } else {
         launch_join(r, plan, jl);
       }
       tm.tick(kStJoin);
-      launch_offer(r, plan, q_key_p, q_tgt_p, q_fill.p,
+      launch_offer(r, plan, q_key_p, q_tgt_p, q_fill_p,
                    (u32)ceil_div<u64>(jl.p_hi - jl.p_lo, (u64)kJoinChunk), slots_p, S, nb, ways,
-                   counters.p, jl.p_lo, jl.n_live);
+                   counters_p, jl.p_lo, jl.n_live);
       tm.tick(kStOffer);
       launches += 2;
     }
-    k_apply<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst.p, slots_p,
-                                                   counters.p, use_tc ? ds.x : nullptr, ds.d);
+    k_apply<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst_p, slots_p,
+                                                   counters_p, use_tc ? ds.x : nullptr, ds.d);
     KNNG_LAUNCH_CHECK();
     launches += 1;
     tm.tick(kStApply);
-    KNNG_CUDA(cudaMemcpyAsync(hcount.p, counters.p, kNumCounters * sizeof(u64),
+    KNNG_CUDA(cudaMemcpyAsync(hcount.p, counters_p, kNumCounters * sizeof(u64),
                               cudaMemcpyDeviceToHost, r.stream));
     // busy-poll the iteration's end: a sleeping cudaStreamSynchronize woke
     // up late now and then, idling the GPU before the next iteration (up to

@@ -72,9 +72,31 @@ void validate_nnd(const NndParams& p, uint64_t n);
 // Grow-only buffers of a build (offer queue, candidate buckets, join lists),
 // kept by a context across builds on one device: a fresh ~50 GB set per build
 // occasionally made the pool map memory anew while the GPU waited.
+struct SampleLists {
+  uint32_t bound = 0;
+  DBuf<uint32_t> nf, nfn, of, ofn, nr, nrn, orv, orn;
+};
+// reverse-list scratch of one sampling pass (counts, offsets, pair buffers)
+struct RevCsr {
+  DBuf<uint32_t> cnt_new, cnt_old, src_cnt, cur_new, cur_old, long_cnt, long_rec;
+  DBuf<uint64_t> off_new, off_old, src_off_new, src_off_old;
+  DBuf<uint32_t> key_new, val_new, key_old, val_old, tk_new, tv_new, tk_old, tv_old;
+};
+
 struct NndWorkspace {
   DBuf<uint64_t> q_key, slots;
   DBuf<uint32_t> q_tgt, L_ids;
+  // every other per-build buffer, so a build in a warm context issues no
+  // allocation and no memory query (sized for the largest n / k / B seen)
+  SampleLists lists;
+  RevCsr rev;
+  uint64_t lists_n = 0;
+  uint32_t lists_k = 0, lists_b = 0;
+  DBuf<float> worst;
+  DBuf<uint64_t> counters, act_off;
+  DBuf<uint32_t> L_cnt, act, act_flag, q_fill, chunk_ctr;
+  uint64_t q_chunks_per_slice = 0;  // offer-queue slicing decided once per shape
+  uint64_t q_per_chunk = 0, q_n = 0;
 };
 
 // Full build.  keys/flags must hold n*k / n entries on the runner's device.
@@ -86,10 +108,6 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
 void init_random_graph_device(Runner& r, const DevRows& ds, uint32_t k, uint64_t seed,
                               uint64_t* keys, uint32_t* flags);
 
-struct SampleLists {
-  uint32_t bound = 0;
-  DBuf<uint32_t> nf, nfn, of, ofn, nr, nrn, orv, orn;
-};
 void sample_neighbors_device(Runner& r, uint64_t n, uint32_t k, double rho, uint64_t seed,
                              uint64_t iter, const uint64_t* keys, uint32_t* flags,
                              SampleLists& out);

@@ -119,11 +119,14 @@ def test_rank_failure_propagates(knng, tmp_path, world, mode):
     naming it, promptly), and a rank that never arrives trips the watchdog
     (WorldError) instead of hanging its peers."""
     import json
+    import time
 
     import torch.multiprocessing as mp
     ctx = mp.start_processes(_fail_main, args=(world, _free_port(), str(tmp_path), mode),
                              nprocs=world, join=False, start_method="spawn")
-    ctx.join(timeout=240)
+    t0 = time.time()
+    while not ctx.join(timeout=5) and time.time() - t0 < 240:
+        pass
     res = [json.load(open(tmp_path / f"r{r}.json")) for r in range(world)]
     if mode == "abort":
         assert "injected failure at rank 1" in res[1]["outcome"], res

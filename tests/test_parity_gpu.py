@@ -523,3 +523,42 @@ def test_phase_drivers_chain_equals_pipeline(knng, golden):
     ga, _, _, _ = knng.refine_phase(x, cfg, off, g["local4_ids"], g["local4_d"],
                                     "all_to_all_refine")
     assert np.array_equal(ga.ids, g["a2a4_ids"])
+
+
+@pytest.mark.parametrize("n,d,dist,cl,k", [(20000, 16, "clustered", 4, 16),
+                                           (60000, 32, "clustered", 16, 32),
+                                           (30000, 8, "uniform", 0, 10)])
+def test_reverse_lists_scatter_equals_sorted(knng, n, d, dist, cl, k):
+    """Inside nn_descent the reverse lists are scattered (no sort) and long ones
+    sampled by rank; the graph must equal the stable-radix-sort path's (the
+    reference's transpose order, nndescent.cpp:108-127) bit for bit."""
+    x = knng.gen_random_dataset(n, d, dist, 42, cl)
+    try:
+        os.environ["KNNG_REV_SORT"] = "1"
+        a = knng.nn_descent(x, k=k, seed=5)
+        os.environ["KNNG_REV_SORT"] = "0"
+        b = knng.nn_descent(x, k=k, seed=5)
+    finally:
+        del os.environ["KNNG_REV_SORT"]
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(bits(a.dists), bits(b.dists))
+
+
+def test_reverse_lists_hub_segment(knng):
+    """A hub (the centre of points on a sphere is everyone's nearest
+    neighbour): its reverse segments run to thousands of entries and take the
+    global-memory ranking path; still bit-identical to the sorted path."""
+    rng = np.random.default_rng(3)
+    v = rng.normal(size=(6000, 96)).astype(np.float32)
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    v[0] = 0.0
+    try:
+        os.environ["KNNG_REV_SORT"] = "1"
+        a = knng.nn_descent(v, k=16, seed=1)
+        os.environ["KNNG_REV_SORT"] = "0"
+        b = knng.nn_descent(v, k=16, seed=1)
+    finally:
+        del os.environ["KNNG_REV_SORT"]
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(bits(a.dists), bits(b.dists))
+    # unit vectors in 96-d sit ~sqrt(2) apart, the centre at distance 1: the
+    # hub is in (almost) every row
+    assert (b.ids[1:] == 0).any(axis=1).mean() > 0.95
