@@ -3,13 +3,13 @@
 //   k_join_lists  warp per point: build_join_lists (:135-153) -- new = nf U nr,
 //                 old = (of U orv) \ new, first occurrence wins -- written
 //                 compactly (L_ids[p * RMAX ..], L_cnt[p] = nn | na << 16).
-//   k_join        one persistent CTA per SM, a software pipeline over batches
-//                 of points: while batch b is computed from one smem buffer,
-//                 the feature rows of batch b+1 stream into the other with
-//                 cp.async (16 B, coalesced per row).  A batch packs as many
-//                 points as fit (~175 rows of 128-d); its 4x4 micro-tiles --
-//                 a triangle of new x new blocks plus the new x old rectangle
-//                 of every point, rows interleaved so consecutive threads read
+//   k_join        persistent CTAs (two per SM), a software pipeline over
+//                 batches of points: while batch b is computed from one smem
+//                 buffer, the feature rows of batch b+1 stream into the other
+//                 with cp.async (16 B, coalesced per row).  A batch packs as
+//                 many points as fit; its 4x4 micro-tiles -- per point a
+//                 trapezoid of 4-entry blocks (new blocks x all blocks, j > i;
+//                 see tiles_of), rows interleaved so consecutive threads read
 //                 consecutive smem rows (conflict-free LDS.128) -- are spread
 //                 over all 256 threads.  Distances are exact-order (common.cuh),
 //                 filtered by the worst snapshot (nndescent.hpp:39-40) and the
@@ -241,22 +241,34 @@ struct JoinArgs {
   u64* counters;
 };
 
-__device__ __forceinline__ int tri_count(int rt) { return rt * (rt + 1) / 2; }
+// Tiling of one point's pairs (nndescent.cpp:157-171: new x new with i < j,
+// new x old).  The point's list (new entries, then old) is cut into blocks of
+// 4 logical entries; block b of the list pairs with blocks b' >= b: a
+// "trapezoid" of 4x4 micro-tiles over rows = the new blocks (RT of them) and
+// columns = all blocks (CT), rt*ct - rt(rt-1)/2 tiles.  A pair (i, j) of
+// logical entries is evaluated iff i < nn, j < na and j > i -- every new x new
+// pair once (as i < j), every new x old pair once.  Merging the new and old
+// column ranges leaves one padded column block per point (the separate
+// triangle + rectangle of round 1 padded both, ~15% more tile slots).
+// smem layout of a point: logical entry e = 4 blk + w sits at slot w*CT + blk,
+// so micro-tile rows {4 ti + r} are slots ti + CT r and consecutive tiles of a
+// thread row read consecutive smem rows (conflict-free LDS.128).
 __device__ __forceinline__ int tiles_of(u32 cnt) {
   const int nn = cnt & 0xffff, na = cnt >> 16;
-  const int rt = (nn + 3) >> 2, cto = (na - nn + 3) >> 2;
-  return (nn == 0 || na < 2) ? 0 : tri_count(rt) + rt * cto;
+  const int rt = (nn + 3) >> 2, ct = (na + 3) >> 2;
+  return (nn == 0 || na < 2) ? 0 : rt * ct - rt * (rt - 1) / 2;
 }
+// smem rows one point takes (4 CT, padding slots included)
+__device__ __forceinline__ int slots_of(u32 cnt) { return (((int)(cnt >> 16) + 3) >> 2) * 4; }
 
-// A 4x4 micro-tile of one point: rows = new entries ti + RT*r, columns = new
-// entries tj + RT*c (triangle part) or old entries tj + CTo*c (rectangle).
+// A 4x4 micro-tile of one point: rows = logical entries 4 ti + r (slots
+// ti + CT r), columns = logical entries 4 tj + c (slots tj + CT c), tj >= ti.
 struct Tile {
   int pt;          // point slot in the chunk (-1: none)
   int row0, rstr;  // batch smem row of row 0, stride
   int col0, cstr;  // batch smem row of column 0, stride
-  int nn, no;
+  int nn, na;
   int ti, tj;
-  bool tri;
 };
 
 // per meta slot (2): s_ids[G*RMAX] u32 | s_cnt[G] | s_pid[G] | hdr[4]
@@ -365,7 +377,7 @@ __device__ void form_batch(const JoinArgs& a, const Smem& s, int q, int m, int j
       const u32 c = s.cnt(m)[je];
       const int tt = tiles_of(c);
       const int avail = tt - (je == jb ? t0 : 0);
-      const int na = tt ? (int)(c >> 16) : 0;
+      const int na = tt ? slots_of(c) : 0;
       if (je > jb && rows + na > a.RB) {  // rows full: the next batch opens at je
         jn = je;
         break;
@@ -399,6 +411,10 @@ __device__ void form_batch(const JoinArgs& a, const Smem& s, int q, int m, int j
     s.dhdr(q)[3] = t0;
     s.dhdr(q)[4] = jn;
     s.dhdr(q)[5] = tn;
+    int real = 0;  // list rows staged (padding slots excluded): the algorithmic rows
+    for (int j = jb; j < je; ++j)
+      if (tiles_of(s.cnt(m)[j])) real += (int)(s.cnt(m)[j] >> 16);
+    s.dhdr(q)[6] = real;
   }
 }
 
@@ -416,7 +432,13 @@ __device__ void fill_rowids(const JoinArgs& a, const Smem& s, int q) {
       const int mid = (lo + hi + 1) >> 1;
       if (rb[mid] <= r) lo = mid; else hi = mid - 1;
     }
-    rowid[r] = s.ids(m)[lo * a.RMAX + (r - rb[lo])];
+    // slot -> logical entry (slot = w * CT + blk holds entry 4 blk + w); the
+    // padding slots of the last block stage the point's first row (unused)
+    const u32 c = s.cnt(m)[lo];
+    const int na = (int)(c >> 16), ct = (na + 3) >> 2;
+    const int slot = r - rb[lo];
+    const int e = (slot % ct) * 4 + slot / ct;
+    rowid[r] = s.ids(m)[lo * a.RMAX + (e < na ? e : 0)];
   }
 }
 
@@ -458,33 +480,21 @@ __device__ __forceinline__ Tile decode_tile(const Smem& s, int q, int t) {
   while (j + 1 < je && s.tb(q)[j + 1] <= t) ++j;
   const u32 c = s.cnt(m)[j];
   const int nn = c & 0xffff, na = c >> 16;
-  const int rt = (nn + 3) >> 2, no = na - nn, cto = (no + 3) >> 2;
+  const int ct = (na + 3) >> 2;
   int lt = t - s.tb(q)[j] + (j == jb ? s.dhdr(q)[3] : 0);
+  int ti = 0;  // row block ti owns the tiles tj = ti .. ct-1
+  while (lt >= ct - ti) {
+    lt -= ct - ti;
+    ++ti;
+  }
   T.pt = j;
   T.nn = nn;
-  T.no = no;
-  T.rstr = rt;
-  if (lt < tri_count(rt)) {
-    int ti = 0;
-    while (lt >= rt - ti) {
-      lt -= rt - ti;
-      ++ti;
-    }
-    T.tri = true;
-    T.ti = ti;
-    T.tj = ti + lt;
-    T.row0 = s.rb(q)[j] + ti;
-    T.col0 = s.rb(q)[j] + T.tj;
-    T.cstr = rt;
-  } else {
-    lt -= tri_count(rt);
-    T.tri = false;
-    T.ti = lt / cto;
-    T.tj = lt - T.ti * cto;
-    T.row0 = s.rb(q)[j] + T.ti;
-    T.col0 = s.rb(q)[j] + nn + T.tj;
-    T.cstr = cto;
-  }
+  T.na = na;
+  T.ti = ti;
+  T.tj = ti + lt;
+  T.row0 = s.rb(q)[j] + ti;
+  T.col0 = s.rb(q)[j] + T.tj;
+  T.rstr = T.cstr = ct;
   return T;
 }
 
@@ -549,7 +559,7 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
         for (int r = 0; r < 4; ++r)
 #pragma unroll
           for (int c = 0; c < 4; ++c) acc[t][r][c] = 0.0f;
-      if (tid == 0) my_rows += (u64)s.rb(cq)[s.dhdr(cq)[2]];
+      if (tid == 0) my_rows += (u64)s.dhdr(cq)[6];
     }
     {
       const float* xb = s.x(cbuf);
@@ -598,27 +608,23 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
         // ids, worst snapshots (and cosine norm chains) of the tile's 4 rows and 4 columns
         u32 rid[4], cid[4];
         float rw[4], cw[4], rn[4], cn[4];
-        const int cbase = T[t].tri ? 0 : T[t].nn;
-        const int clim = T[t].tri ? T[t].nn : T[t].no;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          const int i = T[t].ti + T[t].rstr * q4, jj = T[t].tj + T[t].cstr * q4;
+          const int i = 4 * T[t].ti + q4, jj = 4 * T[t].tj + q4;
           rid[q4] = i < T[t].nn ? s.ids(m)[lb + i] : 0u;
-          cid[q4] = jj < clim ? s.ids(m)[lb + cbase + jj] : 0u;
+          cid[q4] = jj < T[t].na ? s.ids(m)[lb + jj] : 0u;
           rw[q4] = i < T[t].nn ? __ldg(a.worst + rid[q4]) : 0.0f;
-          cw[q4] = jj < clim ? __ldg(a.worst + cid[q4]) : 0.0f;
+          cw[q4] = jj < T[t].na ? __ldg(a.worst + cid[q4]) : 0.0f;
           rn[q4] = kCos ? __ldg(a.nrm + rid[q4]) : 0.0f;
           cn[q4] = kCos ? __ldg(a.nrm + cid[q4]) : 0.0f;
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const int i = T[t].ti + T[t].rstr * r;
+          const int i = 4 * T[t].ti + r;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const int jj = T[t].tj + T[t].cstr * c;
-            const bool valid =
-                T[t].tri ? (i < T[t].nn && jj < T[t].nn && (T[t].ti < T[t].tj || r < c))
-                         : (i < T[t].nn && jj < T[t].no);
+            const int jj = 4 * T[t].tj + c;
+            const bool valid = i < T[t].nn && jj < T[t].na && jj > i;
             if (!valid) continue;
             const float dist = m_finish<kCos>(acc[t][r][c], rn[r], cn[c]);
             acc[t][r][c] = dist;
@@ -654,10 +660,8 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
           u32 u = 0, v = 0;
           float dist = 0.0f;
           if (two) {
-            const int i = T[t].ti + T[t].rstr * r;
-            const int jj = T[t].tj + T[t].cstr * c;
-            u = s.ids(m)[lb + i];
-            v = s.ids(m)[lb + (T[t].tri ? jj : T[t].nn + jj)];
+            u = s.ids(m)[lb + 4 * T[t].ti + r];
+            v = s.ids(m)[lb + 4 * T[t].tj + c];
             dist = acc[t][r][c];
           }
 #pragma unroll
@@ -747,7 +751,8 @@ JoinPlan plan_join(const Runner& r, int d, uint32_t k, uint32_t B) {
   // kJCtas CTAs must fit one SM (1 KB reserved per CTA)
   smem_max = std::min(smem_max, smem_sm / kJCtas - 1024);
   while (rb > 0 && join_smem_bytes(p.RMAX, rb, p.DCP) + 1024 > (size_t)smem_max) rb -= 8;
-  require(rb >= max_rows, "nn_descent: feature rows too wide for the join's smem batches");
+  // a point takes up to RMAX smem rows (its list, padded to whole 4-blocks)
+  require(rb >= p.RMAX, "nn_descent: feature rows too wide for the join's smem batches");
   p.RB = rb;
   p.smem = join_smem_bytes(p.RMAX, p.RB, p.DCP);
   KNNG_CUDA(cudaFuncSetAttribute(k_join<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
