@@ -1,5 +1,5 @@
 """Per-launch DRAM traffic of k_join from an ncu --metrics csv log (all launches of
-one build): writes profiles/r01_join_traffic.json for bench.py's roofline.traffic.
+one build): writes profiles/join_traffic.json for bench.py's roofline.traffic.
 usage: join_traffic.py <ncu.csv> <capture description> [iterations]
 
 With [iterations] given, the captured launches are one whole build: under ncu's
@@ -30,7 +30,8 @@ out = {"kernel": "k_join", "launches": len(L), "per": div, "capture": sys.argv[2
        "duration_ms": ms, "per_launch": [{"read": d["dram__bytes_read.sum"],
                                           "write": d["dram__bytes_write.sum"],
                                           "ms": d["gpu__time_duration.sum"]} for d in L],
-       "summary": "profiles/r01_join_ncu_full_v3.txt"}
+       "traffic_bytes_per_launch": rd + wr,
+       "summary": sys.argv[4] if len(sys.argv) > 4 else None}
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-json.dump(out, open(os.path.join(root, "profiles", "r01_join_traffic.json"), "w"), indent=1)
+json.dump(out, open(os.path.join(root, "profiles", "join_traffic.json"), "w"), indent=1)
 print(json.dumps({k: v for k, v in out.items() if k != "per_launch"}))
