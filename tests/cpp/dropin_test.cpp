@@ -236,5 +236,34 @@ int main() {
     std::filesystem::remove(path);
   });
   std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "ALL PASS", g_fail);
+  run("u8 dataset through the drop-in (Dataset::view passes u8 rows; l2_u8 core.hpp:32-39)", [] {
+    // a .bvecs-style u8 dataset: nn_descent and brute force on the GPU; every
+    // stored distance must equal the host exact-order l2_u8 of the same rows,
+    // and the u8 build must equal the build of its f32 promotion bit for bit
+    Dataset u = Dataset::empty(16, ElemKind::u8, MetricKind::l2);
+    u.num_points = 3000;
+    Rng rng(11);
+    for (std::size_t i = 0; i < u.num_points * u.dims; ++i)
+      u.u8.push_back(static_cast<std::uint8_t>(rng.next_below(256)));
+    Dataset f = Dataset::empty(16, ElemKind::f32, MetricKind::l2);
+    f.num_points = u.num_points;
+    for (auto v : u.u8) f.f32.push_back(static_cast<float>(v));
+    NnDescentParams p;
+    p.k = 10;
+    p.seed = 4;
+    const KnnGraph gu = nn_descent(u, p), gf = nn_descent(f, p);
+    require(gu.ids == gf.ids && gu.dists == gf.dists, "u8 build != f32-promoted build");
+    check_graph_invariants(gu);
+    for (std::size_t r = 0; r < u.num_points; r += 37)
+      for (std::size_t j = 0; j < p.k; ++j)
+        require(gu.dists_row(r)[j] == u.row_distance(r, gu.ids_row(r)[j]),
+                "stored distance != l2_u8");
+    const GroundTruth gt = brute_force_knng(u, 10);
+    for (std::size_t r = 0; r < u.num_points; r += 101)
+      for (std::size_t j = 0; j < 10; ++j)
+        require(gt.graph.dists_row(r)[j] == u.row_distance(r, gt.graph.ids_row(r)[j]),
+                "brute-force distance != l2_u8");
+    require(recall_at_k(gu, gt, 10) > 0.9, "u8 recall");
+  });
   return g_fail ? 1 : 0;
 }
