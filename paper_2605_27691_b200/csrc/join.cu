@@ -365,55 +365,82 @@ __device__ bool load_chunk(const JoinArgs& a, const Smem& s, int m) {
   return true;
 }
 
-// Thread 0 packs the tiles of meta slot m, starting at tile t0 of point jb,
+// Warp 0 packs the tiles of meta slot m, starting at tile t0 of point jb,
 // into desc slot q: whole points while rows fit, and the tile budget is filled
 // exactly -- a point whose tiles do not all fit is split, the rest of it opens
 // the next batch (its rows are staged in both; every tile is computed once).
+// Lane l looks at point jb + l (a chunk has <= 32 points): inclusive warp
+// scans of rows and tiles give the first point that overflows either budget
+// -- the same cut as a serial walk, in log2(32) steps instead of a
+// single-thread loop the other 255 threads wait for at the next barrier.
 __device__ void form_batch(const JoinArgs& a, const Smem& s, int q, int m, int jb, int t0) {
-  if (threadIdx.x == 0) {
-    const int np = s.mhdr(m)[1];
-    int rows = 0, tiles = 0, je = jb, jn = np, tn = 0;
-    while (je < np) {
-      const u32 c = s.cnt(m)[je];
-      const int tt = tiles_of(c);
-      const int avail = tt - (je == jb ? t0 : 0);
-      const int na = tt ? slots_of(c) : 0;
-      if (je > jb && rows + na > a.RB) {  // rows full: the next batch opens at je
-        jn = je;
-        break;
-      }
-      if (tiles + avail > kMaxTiles) {
-        const int take = kMaxTiles - tiles;
-        if (take <= 0) {
-          jn = je;
-          break;
-        }
-        s.rb(q)[je] = rows;
-        s.tb(q)[je] = tiles;
-        rows += na;
-        tiles += take;
-        jn = je;
-        tn = (je == jb ? t0 : 0) + take;
-        ++je;
-        break;
-      }
-      s.rb(q)[je] = rows;
-      s.tb(q)[je] = tiles;
-      rows += na;
-      tiles += avail;
-      ++je;
+  static_assert(G <= 32, "form_batch: one lane per chunk point");
+  if (threadIdx.x >= 32) return;
+  const unsigned lane = lane_id();
+  const int np = s.mhdr(m)[1];
+  const int j = jb + (int)lane;
+  const bool live = j < np;
+  const u32 c = live ? s.cnt(m)[j] : 0u;
+  const int tt = live ? tiles_of(c) : 0;
+  const int avail = tt - (lane == 0 ? t0 : 0);
+  const int rows_j = tt ? slots_of(c) : 0;
+  int R = rows_j, T = avail;  // inclusive prefix sums
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int r = __shfl_up_sync(kFull, R, o), t = __shfl_up_sync(kFull, T, o);
+    if ((int)lane >= o) {
+      R += r;
+      T += t;
     }
-    s.rb(q)[je] = rows;
-    s.tb(q)[je] = tiles;
+  }
+  // first overflowing point: rows (never the batch's first point) or tiles
+  const unsigned rcut = __ballot_sync(kFull, live && lane > 0 && R > a.RB);
+  const unsigned tcut = __ballot_sync(kFull, live && T > kMaxTiles);
+  const int lr = rcut ? __ffs(rcut) - 1 : 32, lt = tcut ? __ffs(tcut) - 1 : 32;
+  const int live_n = np - jb;
+  int ncnt, jn, tn = 0, take = -1;
+  if (lr <= lt) {  // rows full (or the chunk ends) before the tile budget
+    ncnt = min(lr, live_n);
+    jn = jb + ncnt;
+  } else {          // tile budget: point lt is split (or excluded when nothing fits)
+    const int before = __shfl_sync(kFull, T - avail, lt);  // tiles before point lt
+    take = kMaxTiles - before;
+    if (take <= 0) {
+      ncnt = lt;
+      jn = jb + lt;
+    } else {
+      ncnt = lt + 1;
+      jn = jb + lt;
+      tn = (lt == 0 ? t0 : 0) + take;
+    }
+  }
+  // exclusive prefixes = the points' first row / tile in the batch
+  const int Rx = R - rows_j, Tx = T - avail;
+  if ((int)lane < ncnt) {
+    s.rb(q)[j] = Rx;
+    s.tb(q)[j] = Tx;
+  }
+  const int last = ncnt - 1;
+  int rows_end = 0, tiles_end = 0;
+  if (ncnt > 0) {
+    rows_end = __shfl_sync(kFull, R, last);
+    tiles_end = __shfl_sync(kFull, Tx, last) +
+                (take > 0 && last == lt ? take : __shfl_sync(kFull, avail, last));
+  }
+  // list rows staged (padding slots excluded): the algorithmic rows
+  int real = (int)lane < ncnt && tt ? (int)(c >> 16) : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) real += __shfl_xor_sync(kFull, real, o);
+  if (lane == 0) {
+    const int je = jb + ncnt;
+    s.rb(q)[je] = rows_end;
+    s.tb(q)[je] = tiles_end;
     s.dhdr(q)[0] = m;
     s.dhdr(q)[1] = jb;
     s.dhdr(q)[2] = je;
     s.dhdr(q)[3] = t0;
     s.dhdr(q)[4] = jn;
     s.dhdr(q)[5] = tn;
-    int real = 0;  // list rows staged (padding slots excluded): the algorithmic rows
-    for (int j = jb; j < je; ++j)
-      if (tiles_of(s.cnt(m)[j])) real += (int)(s.cnt(m)[j] >> 16);
     s.dhdr(q)[6] = real;
   }
 }
