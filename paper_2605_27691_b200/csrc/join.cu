@@ -131,12 +131,17 @@ __global__ __launch_bounds__(256) void k_join_lists(u64 n, u32 k, u32 B, int RMA
 #endif
 constexpr int kOfferBatch = KNNG_OFFER_BATCH;  // offers per thread (independent atomics per round)
 
+// Targets outside [t_lo, t_hi) are skipped: the offers of a slice are resolved
+// in target-range passes whose bucket rows stay L2-resident (plan in
+// launch_offer), turning random DRAM sectors into L2 hits for the price of
+// re-reading the 4-byte target array once per pass.
 __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
                                                const u32* __restrict__ q_tgt,
                                                const u32* __restrict__ q_fill, u64 q_per_chunk,
                                                u32 chunks, u64* __restrict__ slots, u32 S,
                                                u32 nb, u32 ways, u64* __restrict__ counters,
-                                               u64 p_lo, const u64* __restrict__ n_live) {
+                                               u64 p_lo, const u64* __restrict__ n_live,
+                                               u32 t_lo, u32 t_hi) {
   if (n_live) {  // the slice's live chunk count, read on the device
     const u64 live = *n_live;
     const u64 hi = live < p_lo ? 0 : live - p_lo;
@@ -145,7 +150,7 @@ __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
   }
   for (u32 region = blockIdx.x; region < chunks; region += gridDim.x) {
     const u32 fill = q_fill[region];
-    if (threadIdx.x == 0 && counters)
+    if (threadIdx.x == 0 && counters && t_lo == 0)
       atomicAdd(reinterpret_cast<unsigned long long*>(counters + kCntOfferSeen), (u64)fill);
     const u64 base = (u64)region * q_per_chunk;
     // warp-uniform trip count + __syncwarp: lanes that leave the cascade early
@@ -160,9 +165,11 @@ __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
         const u32 e = e0 + i * blockDim.x;
         bk[i] = nullptr;
         if (e < fill) {
-          key[i] = q_key[base + e];
           const u32 tgt = q_tgt[base + e];
-          bk[i] = slots + (u64)tgt * S + (u64)bucket_hash(tgt, key_id(key[i]), nb) * ways;
+          if (tgt >= t_lo && tgt < t_hi) {
+            key[i] = q_key[base + e];
+            bk[i] = slots + (u64)tgt * S + (u64)bucket_hash(tgt, key_id(key[i]), nb) * ways;
+          }
         }
       }
       // L2-coherent snapshots (L1 lines would go stale under the atomics);
@@ -847,12 +854,25 @@ void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& l) {
 void launch_offer(const Runner& r, const JoinPlan& plan, const uint64_t* q_key,
                   const uint32_t* q_tgt, const uint32_t* q_fill, uint32_t chunks,
                   uint64_t* slots, uint32_t S, uint32_t nb, uint32_t ways, uint64_t* counters,
-                  uint64_t p_lo, const uint64_t* n_live) {
+                  uint64_t p_lo, const uint64_t* n_live, uint64_t n_points) {
   if (!chunks) return;
   const unsigned grid = (unsigned)std::min<uint64_t>(chunks, (uint64_t)r.num_sms * 8);
-  k_offer<<<grid, 256, 0, r.stream>>>(q_key, q_tgt, q_fill, plan.q_per_chunk, chunks, slots, S,
-                                      nb, ways, counters, p_lo, n_live);
-  KNNG_LAUNCH_CHECK();
+  // target-range passes: bucket rows of one pass <= ~48 MB (L2 is 126 MB); at
+  // most 8 passes (beyond that re-reading the targets costs more than the
+  // random sectors it saves -- one pass then)
+  const uint64_t slot_bytes = n_points * (uint64_t)S * 8;
+  uint64_t passes = (slot_bytes + (48ull << 20) - 1) / (48ull << 20);
+  if (const char* v = std::getenv("KNNG_OFFER_PASSES")) passes = std::max(1, std::atoi(v));
+  if (passes > 8 || passes < 1) passes = 1;
+  const uint64_t per = (n_points + passes - 1) / passes;
+  for (uint64_t b = 0; b < passes; ++b) {
+    const u32 lo = (u32)std::min<uint64_t>(b * per, n_points);
+    const u32 hi = (u32)std::min<uint64_t>((b + 1) * per, n_points);
+    k_offer<<<grid, 256, 0, r.stream>>>(q_key, q_tgt, q_fill, plan.q_per_chunk, chunks, slots,
+                                        S, nb, ways, counters, p_lo, n_live, lo,
+                                        passes == 1 ? 0xffffffffu : hi);
+    KNNG_LAUNCH_CHECK();
+  }
 }
 
 }  // namespace knng_b200

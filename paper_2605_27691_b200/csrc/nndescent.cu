@@ -971,7 +971,7 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
       tm.tick(kStJoin);
       launch_offer(r, plan, q_key_p, q_tgt_p, q_fill_p,
                    (u32)ceil_div<u64>(jl.p_hi - jl.p_lo, (u64)kJoinChunk), slots_p, S, nb, ways,
-                   counters_p, jl.p_lo, jl.n_live);
+                   counters_p, jl.p_lo, jl.n_live, n);
       tm.tick(kStOffer);
       launches += 2;
     }

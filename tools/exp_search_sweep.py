@@ -1,10 +1,12 @@
-"""Sweep search smem shapes (KNNG_SEARCH_DCH / KNNG_SEARCH_VIS) in one process
-over the C5-regime 1M graph; checks bit-identity against exact mode."""
+"""Sweep search smem shapes (KNNG_SEARCH_DCH / KNNG_SEARCH_VIS / KNNG_SEARCH_PIPE)
+in one process over a C4/C5-regime graph (clustered(16), beam 128 / 96 entries);
+checks bit-identity against exact mode.  N points, D dims (env)."""
 import os, sys, time, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, paper_2605_27691_b200 as knng
 n = int(os.environ.get("N", "1000000"))
-x = torch.from_numpy(knng.gen_random_dataset(2 * n, 128, "clustered", 42, 16)).cuda()
+d = int(os.environ.get("D", "128"))
+x = torch.from_numpy(knng.gen_random_dataset(2 * n, d, "clustered", 42, 16)).cuda()
 base, qry = x[:n].contiguous(), x[n:].contiguous()
 g = knng.nn_descent(base, knng.NnDescentParams(k=32, seed=1))
 sg = knng.optimize_graph(g, base, 32)
@@ -23,4 +25,8 @@ for cfg in CFGS:
         r = knng.ann_search(qry, sg, base, sp)
         torch.cuda.synchronize(); ts.append(time.perf_counter() - t)
     ok = bool(torch.equal(r.ids, ref.ids)) and bool(torch.equal(r.dists.view(torch.int32), ref.dists.view(torch.int32)))
-    print(json.dumps(dict(dch=cfg[0], vis=cfg[1], pipe=cfg[2], secs=[round(t, 3) for t in ts], qps=n / min(ts), exact_equal=ok)), flush=True)
+    sc = ref.scored.double().sum().item()
+    gbs = (sc * d * 4 + ref.hops.double().sum().item() * 32 * 4) / min(ts) / 1e9
+    print(json.dumps(dict(n=n, d=d, dch=cfg[0], vis=cfg[1], pipe=cfg[2],
+                          secs=[round(t, 3) for t in ts], qps=n / min(ts), exact_equal=ok,
+                          exact_scored_per_query=sc / n, algorithmic_gbs=gbs)), flush=True)
