@@ -131,10 +131,8 @@ __global__ __launch_bounds__(256) void k_join_lists(u64 n, u32 k, u32 B, int RMA
 #endif
 constexpr int kOfferBatch = KNNG_OFFER_BATCH;  // offers per thread (independent atomics per round)
 
-// Targets outside [t_lo, t_hi) are skipped: the offers of a slice are resolved
-// in target-range passes whose bucket rows stay L2-resident (plan in
-// launch_offer), turning random DRAM sectors into L2 hits for the price of
-// re-reading the 4-byte target array once per pass.
+// Targets outside [t_lo, t_hi) are skipped (target-range passes, opt-in via
+// KNNG_OFFER_PASSES; see launch_offer).
 __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
                                                const u32* __restrict__ q_tgt,
                                                const u32* __restrict__ q_fill, u64 q_per_chunk,
@@ -857,13 +855,12 @@ void launch_offer(const Runner& r, const JoinPlan& plan, const uint64_t* q_key,
                   uint64_t p_lo, const uint64_t* n_live, uint64_t n_points) {
   if (!chunks) return;
   const unsigned grid = (unsigned)std::min<uint64_t>(chunks, (uint64_t)r.num_sms * 8);
-  // target-range passes: bucket rows of one pass <= ~48 MB (L2 is 126 MB); at
-  // most 8 passes (beyond that re-reading the targets costs more than the
-  // random sectors it saves -- one pass then)
-  const uint64_t slot_bytes = n_points * (uint64_t)S * 8;
-  uint64_t passes = (slot_bytes + (48ull << 20) - 1) / (48ull << 20);
+  // one pass by default: target-range passes with L2-resident bucket rows
+  // (KNNG_OFFER_PASSES) measured slower on C2 -- 4 passes 71.8 ms, 8 passes
+  // 115 ms per build vs 43.3 ms for one (profiles/r02_offer_passes.md)
+  uint64_t passes = 1;
   if (const char* v = std::getenv("KNNG_OFFER_PASSES")) passes = std::max(1, std::atoi(v));
-  if (passes > 8 || passes < 1) passes = 1;
+  if (passes > 64 || !n_points) passes = 1;
   const uint64_t per = (n_points + passes - 1) / passes;
   for (uint64_t b = 0; b < passes; ++b) {
     const u32 lo = (u32)std::min<uint64_t>(b * per, n_points);
