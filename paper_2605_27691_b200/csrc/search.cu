@@ -32,6 +32,7 @@
 // a batch is the top-`width` of (beam U batch), which is what the reference's
 // sequential beam_insert produces, so results are bit-identical.
 #include "search.hpp"
+#include "locality.hpp"
 
 #include <algorithm>
 #include <cstdlib>
@@ -74,6 +75,7 @@ struct SearchArgs {
   u32* scored_out;
   u32* scored_ids;   // diagnostics: ids in scoring order, scored_cap per query (null: off)
   u64 scored_cap;
+  const u32* qorder;  // processing order of the queries (null: 0..nq-1)
   u64* gtable;  // per-CTA tagged visited tables (gcap slots each), may be null
   u32 gcap;
   u64* counters;  // [0] hops [1] scored [2] overflowed queries / cache resets
@@ -395,7 +397,11 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
   s_ptr[lane] = (u64)(uintptr_t)a.V;
   __syncwarp();
   u64 tot_hops = 0, tot_scored = 0, tot_ovf = 0;
-  for (u64 q = blockIdx.x; q < a.nq; q += gridDim.x) {
+  for (u64 qi = blockIdx.x; qi < a.nq; qi += gridDim.x) {
+    // queries run in a spatial order (concurrent warps walk nearby parts of
+    // the graph and share L2 lines); everything below is indexed by the
+    // query's own id q, so results are unchanged
+    const u64 q = a.qorder ? a.qorder[qi] : qi;
     // stage query, clear visited
     const float* qrow = a.Q + q * (u64)a.d;
     for (int t = lane; t < a.d; t += 32) s_q[t] = qrow[t];
@@ -639,6 +645,14 @@ void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint
   a.scored_out = scored;
   a.scored_ids = scored_ids;
   a.scored_cap = scored_cap;
+  // large batches: a locality order of the queries (KNNG_SEARCH_ORDER=0 off);
+  // 2M C4-shape queries: 0.634 -> 0.586 s (profiles/r02_search_sweep.md)
+  DBuf<u32> qord;
+  if (nq >= 65536 && env_u32("KNNG_SEARCH_ORDER", 1) != 0 && d <= 1024) {
+    qord.alloc(r, nq);
+    locality_order(r, Q, nq, d, 0x5eed04d0ull, qord.p);
+    a.qorder = qord.p;
+  }
   a.id_base = id_base;
   a.vis_slots = sh.vis_slots;
   a.vis_limit = sh.vis_limit;

@@ -562,3 +562,22 @@ def test_reverse_lists_hub_segment(knng):
     # unit vectors in 96-d sit ~sqrt(2) apart, the centre at distance 1: the
     # hub is in (almost) every row
     assert (b.ids[1:] == 0).any(axis=1).mean() > 0.95
+
+
+@pytest.mark.gpu
+def test_ann_search_locality_order_is_invisible(knng, monkeypatch):
+    # >= 65536 queries run in a Morton processing order (search.cu); every
+    # query's result (its entry points are seeded by its index) must equal the
+    # one the given order produces (KNNG_SEARCH_ORDER=0)
+    x = knng.gen_random_dataset(30000, 16, "clustered", 7, 40)
+    g = knng.nn_descent(x, k=16, seed=3)
+    sg = knng.optimize_graph(g, x, 16)
+    q = knng.gen_random_dataset(70000, 16, "clustered", 8, 40)
+    p = knng.SearchParams(10, 48, 16, 0, 5)
+    ordered = knng.ann_search(q, sg, x, p, diagnostics=True)
+    monkeypatch.setenv("KNNG_SEARCH_ORDER", "0")
+    given = knng.ann_search(q, sg, x, p, diagnostics=True)
+    assert np.array_equal(ordered.ids, given.ids)
+    assert np.array_equal(bits(ordered.dists), bits(given.dists))
+    assert np.array_equal(ordered.hops, given.hops)
+    assert np.array_equal(ordered.scored, given.scored)
