@@ -9,8 +9,6 @@
 // keep id order).  Consumers only change the ORDER in which independent work
 // runs (the search: tests bit-identical) or renumber a build internally.
 #include <algorithm>
-#include <cmath>
-#include <vector>
 
 #include "locality.hpp"
 #include "radix.hpp"
@@ -59,6 +57,21 @@ __global__ void k_project(const float* __restrict__ X, u64 n, int d, const float
   }
 }
 
+// seeded projection directions (Box-Muller from the counter-based stream) and
+// the min / max identities: generated on the device, so the call makes no
+// host copy or synchronisation (a build starts its GPU work at once)
+__global__ void k_dirs(u64 seed, int count, float* __restrict__ R, int* __restrict__ mm) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x) {
+    const u64 a = sm64_mix(seed + (2ull * t + 1) * kGamma);
+    const u64 b = sm64_mix(seed + (2ull * t + 2) * kGamma);
+    const float u1 = ((float)(a >> 40) + 1.0f) * (1.0f / 16777217.0f);
+    const float u2 = (float)(b >> 40) * (1.0f / 16777216.0f);
+    R[t] = sqrtf(-2.0f * logf(u1)) * cosf(6.2831853f * u2);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 2 * kAxes)
+    mm[threadIdx.x] = threadIdx.x < kAxes ? 0x7fffffff : (int)0x80000000;
+}
+
 __device__ __forceinline__ float unord(int b) { return __int_as_float(b >= 0 ? b : b ^ 0x7fffffff); }
 
 __global__ void k_morton(const float* __restrict__ P, u64 n, const int* __restrict__ mn,
@@ -93,20 +106,10 @@ void locality_order(const Runner& r, const float* X, uint64_t n, int d, uint64_t
   require(d > 0 && d <= 1024, "locality_order: 1 <= d <= 1024");
   if (n == 0) return;
   DeviceGuard g(r.device);
-  // seeded projection directions (Box-Muller from the counter-based stream)
-  std::vector<float> R((size_t)kAxes * d);
-  for (size_t t = 0; t < R.size(); ++t) {
-    const u64 a = sm64_mix(seed + (2 * t + 1) * kGamma), b = sm64_mix(seed + (2 * t + 2) * kGamma);
-    const double u1 = ((a >> 11) + 1.0) * (1.0 / 9007199254740993.0);
-    const double u2 = (b >> 11) * (1.0 / 9007199254740992.0);
-    R[t] = (float)(std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2));
-  }
-  DBuf<float> dR(r, R.size()), P(r, n * kAxes);
-  KNNG_CUDA(cudaMemcpyAsync(dR.p, R.data(), R.size() * 4, cudaMemcpyHostToDevice, r.stream));
+  DBuf<float> dR(r, (size_t)kAxes * d), P(r, n * kAxes);
   DBuf<int> mm(r, 2 * kAxes);
-  const int init[2 * kAxes] = {0x7fffffff, 0x7fffffff, 0x7fffffff, (int)0x80000000,
-                               (int)0x80000000, (int)0x80000000};
-  KNNG_CUDA(cudaMemcpyAsync(mm.p, init, sizeof(init), cudaMemcpyHostToDevice, r.stream));
+  k_dirs<<<ceil_div(kAxes * d, 256), 256, 0, r.stream>>>(seed, kAxes * d, dR.p, mm.p);
+  KNNG_LAUNCH_CHECK();
   const unsigned grid = (unsigned)std::min<u64>(ceil_div<u64>(n, 256), (u64)r.num_sms * 8);
   k_project<<<grid, 256, 0, r.stream>>>(X, n, d, dR.p, P.p, mm.p, mm.p + kAxes);
   KNNG_LAUNCH_CHECK();
@@ -117,8 +120,6 @@ void locality_order(const Runner& r, const float* X, uint64_t n, int d, uint64_t
   radix_sort_pairs(r, code.p, order, tk.p, tv.p, n, (1u << (kAxes * kBits)) - 1, &in_tmp);
   if (in_tmp)
     KNNG_CUDA(cudaMemcpyAsync(order, tv.p, n * 4, cudaMemcpyDeviceToDevice, r.stream));
-  // HBuf / host copies of R: keep the host vector alive until the copy ran
-  r.sync();
 }
 
 }  // namespace knng_b200

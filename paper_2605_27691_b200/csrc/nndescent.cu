@@ -26,7 +26,9 @@
 #include "nndescent.hpp"
 
 #include <chrono>
+#include "locality.hpp"
 #include "radix.hpp"
+#include "refine_kernels.hpp"
 
 namespace knng_b200 {
 namespace {
@@ -828,9 +830,9 @@ T* ws_buf(Runner& r, DBuf<T>* ws, DBuf<T>& own, uint64_t count) {
 }
 }  // namespace
 
-void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_t* keys,
-                       uint32_t* flags, NndStats* st, bool time_kernels, NndWorkspace* ws) {
-  validate_nnd(p, ds.n);
+namespace {
+void nn_descent_core(Runner& r, const DevRows& ds, const NndParams& p, uint64_t* keys,
+                     uint32_t* flags, NndStats* st, bool time_kernels, NndWorkspace* ws) {
   const u64 n = ds.n;
   const u32 k = p.k;
   const u32 B = bound_of(p.rho, k);
@@ -1021,6 +1023,109 @@ void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_
   if (st) st->launches = launches;
   if (slow_trace_on())
     std::fprintf(stderr, "[knng slow] t %.1f dev %d nnd epilogue done\n", trace_clock_ms(), r.device);
+}
+
+__global__ void k_gather_f32(const float* __restrict__ src, const u32* __restrict__ order, u64 n,
+                             float* __restrict__ dst) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (u64)gridDim.x * blockDim.x)
+    dst[i] = src[order[i]];
+}
+
+// Row i of the renumbered build is point order[i]: relabel its ids, restore
+// the (dist, id) order among equal distances (ties are the only entries the
+// relabelling can reorder) and store it as row order[i], flags following
+// their entries.  One warp per row (k <= 32).
+__global__ __launch_bounds__(256) void k_unrenumber(const u64* __restrict__ kin,
+                                                    const u32* __restrict__ fin,
+                                                    const u32* __restrict__ order, u64 n, u32 k,
+                                                    u64* __restrict__ kout,
+                                                    u32* __restrict__ fout) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 i = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+    u64 key = ~0ull;
+    u32 f = 0;
+    if (lane < k) {
+      key = kin[i * k + lane];
+      if (key != ~0ull) key = (key & 0xffffffff00000000ull) | order[key_id(key)];
+      f = (fin[i] >> lane) & 1u;
+    }
+    // an inversion can only sit between equal distances; sort when one exists
+    const u64 prev = __shfl_up_sync(0xffffffffu, key, 1);
+    if (__any_sync(0xffffffffu, lane > 0 && lane < k && prev > key)) {
+      // bitonic sort of 32 (key, flag) pairs
+      for (unsigned size = 2; size <= 32; size <<= 1)
+        for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+          const u64 ok = __shfl_xor_sync(0xffffffffu, key, stride);
+          const u32 of = __shfl_xor_sync(0xffffffffu, f, stride);
+          const bool up = ((lane & size) == 0);
+          const bool lower = ((lane & stride) == 0);
+          const bool take = lower == up ? ok < key : ok > key;
+          if (take) {
+            key = ok;
+            f = of;
+          }
+        }
+    }
+    const u64 dst = order[i];
+    if (lane < k) kout[dst * k + lane] = key;
+    const u32 bits = __ballot_sync(0xffffffffu, lane < k && f);
+    if (lane == 0) fout[dst] = bits;
+  }
+}
+}  // namespace
+
+// NN-Descent on a locality renumbering of the points: the build runs on the
+// rows permuted into a Morton order of random projections (locality.cu), so
+// a point's neighbours -- and the rows a join tile gathers, the slots an offer
+// hits -- sit close together in HBM.  The renumbered build is a deterministic
+// function of (points, seed) like the plain one (its random streams attach to
+// the new ids); the graph comes back in the caller's numbering and order.
+// C2: 174.1 -> 161.2 ms per build (profiles/r02_renumber.md).
+// KNNG_NND_RENUMBER=0 builds in the given numbering.
+void nn_descent_device(Runner& r, const DevRows& ds, const NndParams& p, uint64_t* keys,
+                       uint32_t* flags, NndStats* st, bool time_kernels, NndWorkspace* ws) {
+  validate_nnd(p, ds.n);
+  const u64 n = ds.n;
+  const char* env = std::getenv("KNNG_NND_RENUMBER");
+  const bool renumber = n >= (1ull << 17) && ds.d <= 1024 && !(env && *env && atoi(env) == 0);
+  if (!renumber) {
+    nn_descent_core(r, ds, p, keys, flags, st, time_kernels, ws);
+    return;
+  }
+  DeviceGuard guard(r.device);
+  const auto t0 = std::chrono::steady_clock::now();
+  const u32 k = p.k;
+  DBuf<u32> order(r, n);
+  locality_order(r, ds.x, n, ds.d, mix_seed(p.seed, 0x10ca11e5ull), order.p);
+  DBuf<float> xr(r, n * (u64)ds.d), nr;
+  gather_rows_device(r, ds.x, ds.d, order.p, n, xr.p);
+  const unsigned g = (unsigned)std::min<u64>(ceil_div<u64>(n, 256), (u64)r.num_sms * 32);
+  if (ds.nrm) {
+    nr.alloc(r, n);
+    k_gather_f32<<<g, 256, 0, r.stream>>>(ds.nrm, order.p, n, nr.p);
+    KNNG_LAUNCH_CHECK();
+  }
+  DBuf<u64> kr(r, n * k);
+  DBuf<u32> fr(r, n);
+  const double pre_ms = time_kernels
+                            ? (r.sync(), 1e3 * std::chrono::duration<double>(
+                                               std::chrono::steady_clock::now() - t0).count())
+                            : 0.0;
+  nn_descent_core(r, DevRows{xr.p, n, ds.d, ds.nrm ? nr.p : nullptr}, p, kr.p, fr.p, st,
+                  time_kernels, ws);
+  const auto t1 = std::chrono::steady_clock::now();
+  k_unrenumber<<<warp_grid(r, n), 256, 0, r.stream>>>(kr.p, fr.p, order.p, n, k, keys, flags);
+  KNNG_LAUNCH_CHECK();
+  if (st) st->launches += 6;
+  if (time_kernels && st) {
+    r.sync();
+    const double post_ms =
+        1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    st->stage_ms[kStInit] += pre_ms + post_ms;
+    st->total_ms += pre_ms + post_ms;
+  }
 }
 
 void export_graph_device(const Runner& r, const uint64_t* keys, const uint32_t* flags,

@@ -41,6 +41,11 @@ void trace(size_t rank, const char* what) {
                        1e3 * (now_s() - g_trace_t0));
 }
 
+// KNNG_TRACE=2: also stamps inside phases, after draining the rank's stream
+// (diagnosis only: it removes the overlap of the stamped steps)
+struct RankState;
+void trace_synced(RankState& R, const char* what);
+
 const char* kDataset = "dataset";
 const char* kGraph = "graph";
 const char* kSGraph = "sgraph";
@@ -119,6 +124,16 @@ DBuf<float> norms_of(const Shared& S, Runner& r, const float* x, uint64_t n) {
   return out;
 }
 
+void trace_synced(RankState& R, const char* what) {
+  static const bool on = [] {
+    const char* v = std::getenv("KNNG_TRACE");
+    return v && std::atoi(v) >= 2;
+  }();
+  if (!on) return;
+  R.runner->sync();
+  trace(R.rank, what);
+}
+
 void pull_rows(Shared& S, RankState& R, uint64_t j, const char* name, void* dst) {
   S.world->get(R.rank, j, name, dst, *R.runner);
 }
@@ -137,6 +152,7 @@ void search_and_merge(Shared& S, RankState& R, const u32* sg, const float* vec, 
   const DBuf<float> qn = norms_of(S, r, R.local_x.p, R.n_local), vn = norms_of(S, r, vec, nvec);
   ann_search_device(r, R.local_x.p, R.n_local, S.d, sg, (u32)S.od, vec, nvec, S.sp,
                     (u32)id_base, rid.p, rd.p, nullptr, nullptr, &R.sc, 0, qn.p, vn.p);
+  trace_synced(R, "  search");
   merge_results_device(r, R.keys.p, nullptr, R.n_local, (u32)S.k, rid.p, rd.p, (u32)S.ks, 0);
 }
 
@@ -249,7 +265,9 @@ void flat_refine(Shared& S, RankState& R) {
     DBuf<float> vx(r, cnt * S.d);
     for (uint64_t j = grp * gsz; j < (grp + 1) * gsz; ++j)
       pull_rows(S, R, j, kDataset, vx.p + (S.offsets[j] - base) * S.d);
+    trace_synced(R, "flat pulled");
     search_and_merge(S, R, sg.p, vx.p, cnt, base);
+    trace_synced(R, "flat searched");
   }
   r.sync();
 }

@@ -76,6 +76,7 @@ struct SearchArgs {
   u32* scored_ids;   // diagnostics: ids in scoring order, scored_cap per query (null: off)
   u64 scored_cap;
   const u32* qorder;  // processing order of the queries (null: 0..nq-1)
+  unsigned long long* qctr;  // dynamic query fetch counter (null: static slots)
   u64* gtable;  // per-CTA tagged visited tables (gcap slots each), may be null
   u32 gcap;
   u64* counters;  // [0] hops [1] scored [2] overflowed queries / cache resets
@@ -397,7 +398,15 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
   s_ptr[lane] = (u64)(uintptr_t)a.V;
   __syncwarp();
   u64 tot_hops = 0, tot_scored = 0, tot_ovf = 0;
-  for (u64 qi = blockIdx.x; qi < a.nq; qi += gridDim.x) {
+  // query slots: static round robin, or (a.qctr) fetched from a counter so a
+  // CTA that runs ahead takes more queries (no static tail)
+  auto next_q = [&](u64 cur) -> u64 {
+    if (!a.qctr) return cur + gridDim.x;
+    u64 v = 0;
+    if (lane == 0) v = atomicAdd(a.qctr, 1ull);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  for (u64 qi = a.qctr ? next_q(0) : blockIdx.x; qi < a.nq; qi = next_q(qi)) {
     // queries run in a spatial order (concurrent warps walk nearby parts of
     // the graph and share L2 lines); everything below is indexed by the
     // query's own id q, so results are unchanged
@@ -652,6 +661,14 @@ void ann_search_device(Runner& r, const float* Q, uint64_t nq, int d, const uint
     qord.alloc(r, nq);
     locality_order(r, Q, nq, d, 0x5eed04d0ull, qord.p);
     a.qorder = qord.p;
+  }
+  // dynamic query fetch (KNNG_SEARCH_DYN=0: static slots): 5M C4-shape
+  // queries 1.527 -> 1.403 s (tools/exp_search_var.py)
+  DBuf<unsigned long long> qctr;
+  if (env_u32("KNNG_SEARCH_DYN", 1) != 0) {
+    qctr.alloc(r, 1);
+    qctr.zero();
+    a.qctr = qctr.p;
   }
   a.id_base = id_base;
   a.vis_slots = sh.vis_slots;

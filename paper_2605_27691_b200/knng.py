@@ -326,6 +326,14 @@ def _empty_like_mem(x, shape, dtype):
     return np.empty(shape, dtype=dtype)
 
 
+def _itemsize(a) -> int:
+    return a.element_size() if hasattr(a, "element_size") else a.itemsize
+
+
+def _is_contiguous(a) -> bool:
+    return a.is_contiguous() if hasattr(a, "is_contiguous") else a.flags["C_CONTIGUOUS"]
+
+
 def _device_of(x) -> int:
     return x.device.index if _is_torch_cuda(x) else 0
 
@@ -595,8 +603,13 @@ def sample_neighbors(graph: KnnGraph, rho: float, seed: int, iteration: int, dev
 
 
 def nn_descent(x, params: Optional[NnDescentParams] = None, stats: Optional[NnDescentStats] = None,
-               device: Optional[int] = None, metric: str = "l2", **kw) -> KnnGraph:
-    """nn_descent nndescent.cpp:225-259 (lock-free NN-Descent on the B200)."""
+               device: Optional[int] = None, metric: str = "l2", out: Optional[KnnGraph] = None,
+               **kw) -> KnnGraph:
+    """nn_descent nndescent.cpp:225-259 (lock-free NN-Descent on the B200).
+
+    `out`: a KnnGraph to write into (n x k ids u32 / dists f32 / flags u8, or
+    flags None), on the same side as `x` -- e.g. pinned host tensors reused
+    across calls, so the graph comes back by a direct DMA."""
     p = params or NnDescentParams(**kw)
     x = _as_rows(x)
     dev = _device_of(x) if device is None else device
@@ -604,8 +617,18 @@ def nn_descent(x, params: Optional[NnDescentParams] = None, stats: Optional[NnDe
     k = p.k
     if k <= 0 or n <= k:
         raise InvalidArgument("init_random_graph: need 1 <= k < N")
-    g = KnnGraph(_empty_like_mem(x, (n, k), np.uint32), _empty_like_mem(x, (n, k), np.float32),
-                 _empty_like_mem(x, (n, k), np.uint8))
+    if out is None:
+        g = KnnGraph(_empty_like_mem(x, (n, k), np.uint32),
+                     _empty_like_mem(x, (n, k), np.float32),
+                     _empty_like_mem(x, (n, k), np.uint8))
+    else:
+        g = out
+        for a, isz in ((g.ids, 4), (g.dists, 4), (g.flags, 1)):
+            if a is None and isz == 1:
+                continue
+            if tuple(a.shape) != (n, k) or _mem(a) != _mem(x) or _itemsize(a) != isz or \
+                    not _is_contiguous(a):
+                raise InvalidArgument("nn_descent: out must be contiguous n x k on x's side")
     cg = _Graph(_ptr(g.ids), _ptr(g.dists), _ptr(g.flags), n, k, _mem(x))
     ds = _dataset(x, _metric_code(metric))
     cp = p._c()

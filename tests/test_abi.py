@@ -97,6 +97,19 @@ def test_compute_without_gpu_fails_loudly(knng):
         knng.nn_descent(x, k=3)
 
 
+def test_nn_descent_out_validation(knng):
+    # nn_descent(out=...) checks the caller's buffers before any device work
+    x = np.zeros((10, 4), np.float32)
+    bad = [knng.KnnGraph(np.zeros((10, 2), np.uint32), np.zeros((10, 3), np.float32), None),
+           knng.KnnGraph(np.zeros((10, 3), np.uint64), np.zeros((10, 3), np.float32), None),
+           knng.KnnGraph(np.zeros((10, 3), np.uint32), np.zeros((3, 10), np.float32).T, None),
+           knng.KnnGraph(np.zeros((10, 3), np.uint32), np.zeros((10, 3), np.float32),
+                         np.zeros((10, 3), np.uint32))]
+    for g in bad:
+        with pytest.raises(knng.InvalidArgument):
+            knng.nn_descent(x, k=3, out=g)
+
+
 def test_cpp_dropin_compiles(knng):
     """include/knng_b200.hpp (the reference's C++ API over the C-ABI) builds
     and links against libknng_b200.so; tests/cpp/dropin_test.cpp restates

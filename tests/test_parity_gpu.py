@@ -581,3 +581,56 @@ def test_ann_search_locality_order_is_invisible(knng, monkeypatch):
     assert np.array_equal(bits(ordered.dists), bits(given.dists))
     assert np.array_equal(ordered.hops, given.hops)
     assert np.array_equal(ordered.scored, given.scored)
+
+
+@pytest.mark.parametrize("kind", ["f32", "u8_ties"])
+def test_nn_descent_renumbered_build(knng, oracle, monkeypatch, kind):
+    """From 2^17 points nn_descent builds on a Morton renumbering of the rows
+    (nndescent.cu nn_descent_device) and maps the graph back: rows in the
+    caller's numbering, (dist, id) order restored among equal distances
+    (u8_ties: a coarse u8 grid where most rows hold ties), exact distances,
+    deterministic, and the recall of the plain build."""
+    n = 160000
+    if kind == "f32":
+        x = knng.gen_random_dataset(n, 24, "clustered", 11, 64)
+    else:
+        x = np.random.default_rng(5).integers(0, 6, size=(n, 6)).astype(np.uint8)
+    a = knng.nn_descent(x, k=16, seed=4)
+    b = knng.nn_descent(x, k=16, seed=4)
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(bits(a.dists), bits(b.dists))
+    assert oracle.check_invariants(a.ids, a.dists) == 0
+    xf = x.astype(np.float32)
+    rng = np.random.default_rng(2)
+    rows = rng.integers(0, n, 3000)
+    cols = rng.integers(0, 16, 3000)
+    ref = np.array([oracle.l2(xf[r], xf[a.ids[r, c]]) for r, c in zip(rows, cols)], np.float32)
+    assert np.array_equal(bits(a.dists[rows, cols]), bits(ref))
+    monkeypatch.setenv("KNNG_NND_RENUMBER", "0")
+    plain = knng.nn_descent(x, k=16, seed=4)
+    if kind == "f32":
+        sample = np.arange(0, n, 97, dtype=np.uint64)
+        gt, _ = knng.brute_force_knng(x, 10, rows=sample)
+        s = sample.astype(np.int64)
+        assert recall(a.ids[s], gt) >= recall(plain.ids[s], gt) - 0.005
+    else:
+        # ties everywhere: compare the distance profiles (ids are arbitrary among ties)
+        assert abs(float(a.dists.mean()) - float(plain.dists.mean())) < 0.02 * float(plain.dists.mean())
+
+
+def test_nn_descent_into_caller_buffers(knng):
+    # nn_descent(out=...): host (pinned) and device outputs equal the fresh ones
+    torch = pytest.importorskip("torch")
+    x = knng.gen_random_dataset(5000, 16, "clustered", 2, 8)
+    ref = knng.nn_descent(x, k=16, seed=7)
+    pin = lambda t: t.pin_memory().numpy()
+    g = knng.KnnGraph(pin(torch.zeros((5000, 16), dtype=torch.int32)).view(np.uint32),
+                      pin(torch.zeros((5000, 16), dtype=torch.float32)),
+                      pin(torch.zeros((5000, 16), dtype=torch.uint8)))
+    r = knng.nn_descent(x, k=16, seed=7, out=g)
+    assert r is g and np.array_equal(g.ids, ref.ids) and np.array_equal(bits(g.dists), bits(ref.dists))
+    assert np.array_equal(g.flags, ref.flags)
+    xd = torch.from_numpy(x).cuda()
+    gd = knng.KnnGraph(torch.empty((5000, 16), dtype=torch.int32, device="cuda"),
+                       torch.empty((5000, 16), dtype=torch.float32, device="cuda"), None)
+    knng.nn_descent(xd, k=16, seed=7, out=gd)
+    assert np.array_equal(gd.ids.cpu().numpy().view(np.uint32), ref.ids)
