@@ -46,6 +46,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
@@ -244,6 +248,9 @@ struct JoinArgs {
   u64 q_per_chunk;
   int DC, DCP, RB;
   u64* counters;
+  // (-0.0f, -0.0f): the addend of the paired squares' FFMA2 (see sq_pairs);
+  // a kernel argument, so ptxas cannot see it is a no-op addend
+  unsigned long long negz2;
 };
 
 // Tiling of one point's pairs (nndescent.cpp:157-171: new x new with i < j,
@@ -453,6 +460,7 @@ __device__ void form_batch(const JoinArgs& a, const Smem& s, int q, int m, int j
 // Stage dims [c0, c0+dc) of every row of desc q into buffer buf (async).
 // Row -> point id table of desc q (all threads; once per batch).  Row r
 // belongs to the last point j with rb[j] <= r (zero-row points share rb).
+template <bool kPair>
 __device__ void fill_rowids(const JoinArgs& a, const Smem& s, int q) {
   const int m = s.dhdr(q)[0], jb = s.dhdr(q)[1], je = s.dhdr(q)[2];
   const int* rb = s.rb(q);
@@ -469,20 +477,51 @@ __device__ void fill_rowids(const JoinArgs& a, const Smem& s, int q) {
     const u32 c = s.cnt(m)[lo];
     const int na = (int)(c >> 16), ct = (na + 3) >> 2;
     const int slot = r - rb[lo];
-    const int e = (slot % ct) * 4 + slot / ct;
+    int e;
+    if (kPair) {  // slot = 2 pair-row + parity, pair-row = (w >> 1) CT + blk
+      const int pr = slot >> 1, h = pr >= ct;
+      e = (pr - h * ct) * 4 + 2 * h + (slot & 1);
+    } else {
+      e = (slot % ct) * 4 + slot / ct;
+    }
     rowid[r] = s.ids(m)[lo * a.RMAX + (e < na ? e : 0)];
   }
 }
 
 // Stage dims [c0, c0+dc) of every row of desc q into buffer buf (async,
 // one 16-byte cp.async per thread per step, all lanes busy).
+template <bool kPair>
 __device__ void issue_rows(const JoinArgs& a, const Smem& s, int q, int c0, int buf) {
   const int je = s.dhdr(q)[2];
   const int rows = s.rb(q)[je];
   const int dc = min(a.DC, a.d - c0);
   const u32* rowid = s.rowid(q);
   float* xb = s.x(buf);
-  if ((a.d & 3) == 0) {
+  if (kPair) {
+    // pair layout: slots 2i, 2i+1 share pair-row i (stride 2 DCP), their
+    // values interleaved per dim.  Thread -> (pair-row, 4-dim quad): 8
+    // four-byte cp.async fill 32 contiguous smem bytes from 16 B of each
+    // row (one address computation per 8 elements; the quads of a warp
+    // cover whole 128-B row segments, L1-cached across the 8 copies)
+    const int qd = dc >> 2, ppi = kJT / qd;
+    const int p0 = (int)threadIdx.x / qd, q4 = (int)threadIdx.x - p0 * qd;
+    if (p0 < ppi) {
+      const float* src = a.X + c0 + q4 * 4;
+      float* dst = xb + q4 * 8;
+      const uint2* rid2 = reinterpret_cast<const uint2*>(rowid);
+      for (int pr = p0; pr < (rows >> 1); pr += ppi) {
+        const uint2 id = rid2[pr];
+        const float* s0 = src + (u64)id.x * (u64)a.d;
+        const float* s1 = src + (u64)id.y * (u64)a.d;
+        float* d0 = dst + pr * 2 * a.DCP;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          cp_async4(d0 + 2 * k, s0 + k);
+          cp_async4(d0 + 2 * k + 1, s1 + k);
+        }
+      }
+    }
+  } else if ((a.d & 3) == 0) {
     // thread -> (row r0 + k * rpi, 16-byte piece c4): one division per call
     const int qd = dc >> 2, rpi = kJT / qd;
     const int r0 = (int)threadIdx.x / qd, c4 = (int)threadIdx.x - r0 * qd;
@@ -501,6 +540,7 @@ __device__ void issue_rows(const JoinArgs& a, const Smem& s, int q, int c0, int 
   cp_async_commit();
 }
 
+template <bool kPair>
 __device__ __forceinline__ Tile decode_tile(const Smem& s, int q, int t) {
   Tile T;
   const int m = s.dhdr(q)[0], jb = s.dhdr(q)[1], je = s.dhdr(q)[2];
@@ -524,13 +564,43 @@ __device__ __forceinline__ Tile decode_tile(const Smem& s, int q, int t) {
   T.na = na;
   T.ti = ti;
   T.tj = ti + lt;
-  T.row0 = s.rb(q)[j] + ti;
-  T.col0 = s.rb(q)[j] + T.tj;
+  // pair layout: row0 / col0 index pair-rows (entries 4 ti + {0,1} and
+  // 4 ti + {2,3} sit in pair-rows ti and ct + ti of the point)
+  const int base = kPair ? s.rb(q)[j] >> 1 : s.rb(q)[j];
+  T.row0 = base + ti;
+  T.col0 = base + T.tj;
   T.rstr = T.cstr = ct;
   return T;
 }
 
+// Two pairs at once, exact order: T = (b0 - a, b1 - a) with FADD2 (a
+// broadcast; b - a is the exact negation of a - b, so squares are equal),
+// P = T*T + (-0) with FFMA2 (x*y + -0 rounds once, = the rounded product),
+// acc += P with FADD2 -- every pair still sums round(acc + round(t*t)) dim by
+// dim.  A plain FMUL2 + FADD2 would be contracted into FFMA2 by ptxas (one
+// rounding); the runtime -0 addend blocks that.  1.5 instructions per
+// pair-dim instead of 2 (FADD2 sub + FMUL2 + two scalar FADDs per two dims).
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
 template <bool kCos>
+__device__ __forceinline__ void step_pairs(unsigned long long& acc, float a, float b0, float b1,
+                                           unsigned long long negz2) {
+  const unsigned long long A = pack2(a, a), B = pack2(b0, b1);
+  unsigned long long P;
+  if (kCos) {
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(P) : "l"(B), "l"(A), "l"(negz2));
+  } else {
+    unsigned long long T;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(T) : "l"(B), "l"(A));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(P) : "l"(T), "l"(negz2));
+  }
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc) : "l"(acc), "l"(P));
+}
+
+template <bool kCos, bool kPair>
 __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Smem s = carve(smem, a.RMAX, a.RB, a.DCP);
@@ -544,9 +614,9 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
   int cq = 0, cc0 = 0, cbuf = 0;  // current unit: desc slot, dim offset, buffer
   form_batch(a, s, 0, 0, 0, 0);
   __syncthreads();
-  fill_rowids(a, s, 0);
+  fill_rowids<kPair>(a, s, 0);
   __syncthreads();
-  issue_rows(a, s, 0, 0, 0);
+  issue_rows<kPair>(a, s, 0, 0, 0);
 
   Tile T[kTPT];
   float acc[kTPT][4][4];
@@ -568,12 +638,12 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
       }
       __syncthreads();
       if (have_next) {
-        fill_rowids(a, s, nq);
+        fill_rowids<kPair>(a, s, nq);
         __syncthreads();
       }
     }
     if (have_next) {
-      issue_rows(a, s, nq, nc0, nbuf);
+      issue_rows<kPair>(a, s, nq, nc0, nbuf);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -584,7 +654,7 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
     const int m = s.dhdr(cq)[0];
     if (cc0 == 0) {
 #pragma unroll
-      for (int t = 0; t < kTPT; ++t) T[t] = decode_tile(s, cq, tid + t * kJT);
+      for (int t = 0; t < kTPT; ++t) T[t] = decode_tile<kPair>(s, cq, tid + t * kJT);
 #pragma unroll
       for (int t = 0; t < kTPT; ++t)
 #pragma unroll
@@ -593,7 +663,78 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
           for (int c = 0; c < 4; ++c) acc[t][r][c] = 0.0f;
       if (tid == 0) my_rows += (u64)s.dhdr(cq)[6];
     }
-    {
+    if (kPair) {
+      const float* xb = s.x(cbuf);
+      const int dc = min(a.DC, a.d - cc0);  // a multiple of 4 (d % 4 == 0)
+#pragma unroll
+      for (int t = 0; t < kTPT; ++t) {
+        if (T[t].pt < 0) continue;
+        unsigned long long acc2[4][2];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) acc2[r][c] = pack2(acc[t][r][2 * c], acc[t][r][2 * c + 1]);
+        // pair-rows: h = 0 holds entries {0,1} of the block, h = 1 entries {2,3}
+        const float* pa[2];
+        const float* pb[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          pa[h] = xb + (T[t].row0 + T[t].rstr * h) * 2 * a.DCP;
+          pb[h] = xb + (T[t].col0 + T[t].cstr * h) * 2 * a.DCP;
+        }
+        // two dims per 16-B smem word: (e0[j], e1[j], e0[j+1], e1[j+1]) of
+        // each pair-row; groups of 8 dims with immediate offsets off
+        // pointers advanced once per group (dc is a multiple of 4)
+        auto two_dims = [&](const float4 (&va)[2], const float4 (&vb)[2]) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const float4& A = va[r >> 1];
+              const float av = j == 0 ? ((r & 1) ? A.y : A.x) : ((r & 1) ? A.w : A.z);
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                if (j == 0)
+                  step_pairs<kCos>(acc2[r][c], av, vb[c].x, vb[c].y, a.negz2);
+                else
+                  step_pairs<kCos>(acc2[r][c], av, vb[c].z, vb[c].w, a.negz2);
+              }
+            }
+        };
+        const float *a0 = pa[0], *a1 = pa[1], *b0 = pb[0], *b1 = pb[1];
+        const int dc8 = dc & ~7;
+        for (int dd = 0; dd < dc8; dd += 8) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4 va[2] = {*reinterpret_cast<const float4*>(a0 + 4 * u),
+                                  *reinterpret_cast<const float4*>(a1 + 4 * u)};
+            const float4 vb[2] = {*reinterpret_cast<const float4*>(b0 + 4 * u),
+                                  *reinterpret_cast<const float4*>(b1 + 4 * u)};
+            two_dims(va, vb);
+          }
+          a0 += 16;
+          a1 += 16;
+          b0 += 16;
+          b1 += 16;
+        }
+        if (dc8 < dc) {  // 4 more dims
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const float4 va[2] = {*reinterpret_cast<const float4*>(a0 + 4 * u),
+                                  *reinterpret_cast<const float4*>(a1 + 4 * u)};
+            const float4 vb[2] = {*reinterpret_cast<const float4*>(b0 + 4 * u),
+                                  *reinterpret_cast<const float4*>(b1 + 4 * u)};
+            two_dims(va, vb);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            asm("mov.b64 {%0,%1}, %2;" : "=f"(acc[t][r][2 * c]), "=f"(acc[t][r][2 * c + 1])
+                : "l"(acc2[r][c]));
+      }
+    } else {
       const float* xb = s.x(cbuf);
       const int dc = min(a.DC, a.d - cc0);
       const int dc4 = dc & ~3;
@@ -773,7 +914,15 @@ JoinPlan plan_join(const Runner& r, int d, uint32_t k, uint32_t B) {
   int dc = 32;
   if (const char* v = std::getenv("KNNG_JOIN_DC")) dc = std::max(8, (std::atoi(v) + 7) & ~7);
   p.DC = d <= dc ? ((d + 7) & ~7) : dc;
-  p.DCP = p.DC + 4;  // DC % 8 == 0 -> (DCP/4) odd: conflict-free LDS.128 across rows
+  // pair layout (opt-in KNNG_JOIN_PAIR=1, d % 4 == 0): pair-row stride
+  // 2 (DC + 2) floats = DC/2 + 1 16-B units, odd; else row stride DC + 4 =
+  // DC/4 + 1 units, odd -- consecutive (pair-)rows are conflict-free for
+  // LDS.128.  Measured on C2: join 102.8 ms vs 88.0 (the interleaving
+  // 4-byte cp.async staging costs more than the 25% fewer math
+  // instructions save; profiles/r02_join_pair.md)
+  const char* pv = std::getenv("KNNG_JOIN_PAIR");
+  p.pair = (d % 4 == 0) && pv && *pv && std::atoi(pv) != 0;
+  p.DCP = p.pair ? p.DC + 2 : p.DC + 4;
   int smem_max = 0;
   KNNG_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, r.device));
   // largest RB whose footprint fits (2 feature buffers + 2 row-id tables)
@@ -787,12 +936,21 @@ JoinPlan plan_join(const Runner& r, int d, uint32_t k, uint32_t B) {
   require(rb >= p.RMAX, "nn_descent: feature rows too wide for the join's smem batches");
   p.RB = rb;
   p.smem = join_smem_bytes(p.RMAX, p.RB, p.DCP);
-  KNNG_CUDA(cudaFuncSetAttribute(k_join<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)p.smem));
-  KNNG_CUDA(cudaFuncSetAttribute(k_join<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)p.smem));
+  KNNG_CUDA(cudaFuncSetAttribute(k_join<false, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  KNNG_CUDA(cudaFuncSetAttribute(k_join<true, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  KNNG_CUDA(cudaFuncSetAttribute(k_join<false, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  KNNG_CUDA(cudaFuncSetAttribute(k_join<true, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   int per_sm = 0;
-  KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_join<false>, kJT, p.smem));
+  if (p.pair)
+    KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_join<false, true>, kJT,
+                                                            p.smem));
+  else
+    KNNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_join<false, false>, kJT,
+                                                            p.smem));
   p.grid = (unsigned)r.num_sms * (unsigned)std::max(per_sm, 1);
   const uint64_t nn_max = 2ull * B, no_max = (uint64_t)k + B;
   const uint64_t max_offers_pp = 2 * (nn_max * (nn_max - 1) / 2 + nn_max * no_max);
@@ -842,10 +1000,17 @@ void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& l) {
   a.DCP = plan.DCP;
   a.RB = plan.RB;
   a.counters = l.counters;
-  if (a.nrm)
-    k_join<true><<<plan.grid, kJT, plan.smem, r.stream>>>(a);
-  else
-    k_join<false><<<plan.grid, kJT, plan.smem, r.stream>>>(a);
+  a.negz2 = 0x8000000080000000ull;
+  if (plan.pair) {
+    if (a.nrm)
+      k_join<true, true><<<plan.grid, kJT, plan.smem, r.stream>>>(a);
+    else
+      k_join<false, true><<<plan.grid, kJT, plan.smem, r.stream>>>(a);
+  } else if (a.nrm) {
+    k_join<true, false><<<plan.grid, kJT, plan.smem, r.stream>>>(a);
+  } else {
+    k_join<false, false><<<plan.grid, kJT, plan.smem, r.stream>>>(a);
+  }
   KNNG_LAUNCH_CHECK();
 }
 

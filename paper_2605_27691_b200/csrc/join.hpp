@@ -14,6 +14,7 @@ constexpr uint32_t kWays = 4;  // candidate slots per hash bucket
 struct JoinPlan {
   int RMAX = 0;       // list capacity per point (>= 2B + k + B, multiple of 4)
   int DC = 0, DCP = 0;  // dims per staged chunk, smem row stride (floats)
+  int pair = 0;         // pair layout (d % 4 == 0): two rows interleaved per dim
   int RB = 0;         // rows per staged batch
   size_t smem = 0;    // dynamic smem of k_join
   unsigned grid = 0;  // persistent CTAs (one per SM)

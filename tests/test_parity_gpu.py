@@ -634,3 +634,18 @@ def test_nn_descent_into_caller_buffers(knng):
                        torch.empty((5000, 16), dtype=torch.float32, device="cuda"), None)
     knng.nn_descent(xd, k=16, seed=7, out=gd)
     assert np.array_equal(gd.ids.cpu().numpy().view(np.uint32), ref.ids)
+
+
+@pytest.mark.parametrize("n,d,metric", [(20000, 128, "l2"), (30000, 96, "l2"), (8000, 960, "l2"),
+                                        (20000, 12, "l2"), (20000, 64, "cosine"),
+                                        (6000, 36, "cosine")])
+def test_join_pair_layout_bitexact(knng, monkeypatch, n, d, metric):
+    """The join's pair layout (two staged rows interleaved per dim, FADD2 /
+    FFMA2(-0) / FADD2 over two pairs at once) computes the same exact-order
+    distances as the row layout: identical graphs."""
+    x = knng.gen_random_dataset(n, d, "clustered", 31, 20)
+    monkeypatch.setenv("KNNG_JOIN_PAIR", "1")
+    a = knng.nn_descent(x, k=16, seed=2, metric=metric)
+    monkeypatch.setenv("KNNG_JOIN_PAIR", "0")
+    b = knng.nn_descent(x, k=16, seed=2, metric=metric)
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(bits(a.dists), bits(b.dists))
