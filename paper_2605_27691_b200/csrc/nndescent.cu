@@ -525,10 +525,52 @@ __global__ __launch_bounds__(256) void k_rev_select_long(u64 n_src, u32 B,
 // ---------------------------------------------------------------------------
 // apply_candidates nndescent.cpp:199-223 -- warp per point
 // ---------------------------------------------------------------------------
+// The reference inserts a point's buffered candidates with knn_insert in
+// buffer order (core.cpp:99-112: duplicates of row ids and non-improvements
+// rejected, the rest shifted in).  The row it ends with is the k smallest of
+// (row U candidates) whatever the order; the count of accepted inserts
+// depends on the order (a candidate accepted and later pushed out counts).
+// The buffer order is the join threads' arrival order there; here the
+// candidates are applied in ascending key order -- one valid buffer order --
+// for which "accepted" = "kept": the count is the number of new entries the
+// row ends with.
+//
+// Many candidates (early iterations: ~50 per point): two 32-key bitonic
+// sorts, a bitonic merge keeping the 32 smallest candidates and one more
+// merge against the row (with the new-entry flags), ~400 instructions per
+// point.  Few candidates: knn_insert one at a time (~40 each).
+//
 // With X set the buckets hold LOWER BOUNDS of the exact distances (the
 // tensor-core join, join_tc.cu): every candidate whose bound beats the row's
 // current worst gets its exact-order distance recomputed here (core.hpp:23-30),
 // so the inserted keys -- and the decisions of knn_insert -- are exact.
+__device__ __forceinline__ u64 shfl64(u64 v, int src) { return __shfl_sync(kFull, v, src); }
+__device__ __forceinline__ u64 shfl_xor64(u64 v, int m) { return __shfl_xor_sync(kFull, v, m); }
+
+// ascending bitonic sort of one key per lane
+__device__ __forceinline__ u64 warp_sort_asc(u64 v, unsigned lane) {
+#pragma unroll
+  for (unsigned size = 2; size <= 32; size <<= 1)
+#pragma unroll
+    for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+      const u64 o = shfl_xor64(v, stride);
+      const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
+      v = keep_min ? (o < v ? o : v) : (o > v ? o : v);
+    }
+  return v;
+}
+// a bitonic sequence of one key per lane -> ascending
+__device__ __forceinline__ u64 warp_merge_asc(u64 v, unsigned lane) {
+#pragma unroll
+  for (unsigned stride = 16; stride > 0; stride >>= 1) {
+    const u64 o = shfl_xor64(v, stride);
+    v = (lane & stride) == 0 ? (o < v ? o : v) : (o > v ? o : v);
+  }
+  return v;
+}
+
+constexpr u32 kApplySerialMax = 8;  // candidates up to which knn_insert runs one by one
+
 __global__ __launch_bounds__(256) void k_apply(u64 n, u32 k, u32 S, u64* __restrict__ keys,
                                                u32* __restrict__ flags,
                                                float* __restrict__ worst,
@@ -540,60 +582,178 @@ __global__ __launch_bounds__(256) void k_apply(u64 n, u32 k, u32 S, u64* __restr
   u64 acc_total = 0;
   for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); p < n; p += warps) {
     u64* sl = slots + p * S;
-    // cheap skip: any slot filled?
-    u64 rk = kEmptyKey;
+    // the buffer (S <= 64: two keys per lane), reset as it is read
+    u64 c[2];
+    bool any = false;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const u32 si = h * 32 + lane;
+      c[h] = si < S ? sl[si] : kEmptyKey;
+      const bool filled = c[h] != kEmptyKey;
+      if (filled) sl[si] = kEmptyKey;  // CandidateBuffer::reset
+      any |= __any_sync(kFull, filled);
+    }
+    if (!any) continue;
+    u64 rk = lane < k ? keys[p * k + lane] : kEmptyKey;
+    u32 fl = lane < k ? (flags[p] >> lane) & 1u : 0u;
+    const u64 last = shfl64(rk, k - 1);
+    u32 nv = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (X && c[h] < last) {
+        const u32 v = key_id(c[h]);
+        c[h] = pack_key(l2_exact(X + p * (u64)d, X + (u64)v * d, d), v);
+      }
+      if (c[h] >= last) c[h] = kEmptyKey;  // non-improvement (filled or not)
+      // duplicate of a row id: its key equals that row entry's (same exact
+      // distance), found by a binary search of the sorted row
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const u64 x = shfl64(rk, lo + step - 1);
+        if (x < c[h]) lo += step;
+      }
+      const u64 at = shfl64(rk, lo & 31);
+      if (c[h] != kEmptyKey && lo < (int)k && at == c[h]) c[h] = kEmptyKey;
+      nv += __popc(__ballot_sync(kFull, c[h] != kEmptyKey));
+    }
+    if (nv == 0) continue;
+    u32 kept = 0;
+    if (nv <= kApplySerialMax) {
+      // knn_insert one by one (the kept row is order-independent)
+      u32 from_c = 0;
+      u64 lst = last;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        unsigned mask = __ballot_sync(kFull, c[h] != kEmptyKey);
+        while (mask) {
+          const int src = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const u64 cc = shfl64(c[h], src);
+          if (cc >= lst) continue;
+          const u32 pos = __popc(__ballot_sync(kFull, lane < k && rk < cc));
+          const u64 up = __shfl_up_sync(kFull, rk, 1);
+          const u32 upf = __shfl_up_sync(kFull, fl | (from_c << 1), 1);
+          if (lane > pos && lane < k) {
+            rk = up;
+            fl = upf & 1u;
+            from_c = upf >> 1;
+          }
+          if (lane == pos) {
+            rk = cc;
+            fl = 1;
+            from_c = 1;
+          }
+          lst = shfl64(rk, k - 1);
+        }
+      }
+      kept = __popc(__ballot_sync(kFull, lane < k && from_c));
+    } else {
+      // the 32 smallest candidates, ascending: sort both halves, then the
+      // elementwise min of one and the other reversed is bitonic
+      const u64 a = warp_sort_asc(c[0], lane);
+      const u64 b = warp_sort_asc(c[1], lane);
+      const u64 br = shfl64(b, 31 - lane);
+      const u64 cs = warp_merge_asc(a < br ? a : br, lane);
+      // the k smallest of row U candidates (rows pad lanes >= k with empty
+      // keys), new-entry flags following their keys
+      const u64 cr = shfl64(cs, 31 - lane);
+      const bool take_c = cr < rk;
+      u64 v = take_c ? cr : rk;
+      u32 f = take_c ? 3u : fl;  // bit 1: from the candidates
+#pragma unroll
+      for (unsigned stride = 16; stride > 0; stride >>= 1) {
+        const u64 o = shfl_xor64(v, stride);
+        const u32 of = __shfl_xor_sync(kFull, f, stride);
+        const bool lower = (lane & stride) == 0;
+        if (lower ? (o < v) : (o > v)) {
+          v = o;
+          f = of;
+        }
+      }
+      rk = v;
+      fl = f & 1u;
+      kept = __popc(__ballot_sync(kFull, lane < k && (f & 2u)));
+    }
+    if (kept) {
+      if (lane < k) keys[p * k + lane] = rk;
+      const unsigned fmask = __ballot_sync(kFull, fl && lane < k);
+      const u64 nl = shfl64(rk, k - 1);
+      if (lane == 0) {
+        flags[p] = fmask;
+        worst[p] = key_dist(nl);
+      }
+      acc_total += kept;
+    }
+  }
+  if (lane == 0 && acc_total)
+    atomicAdd(reinterpret_cast<unsigned long long*>(counters + kCntAccepted), acc_total);
+}
+
+// More than 64 buffered slots per point (candidate_capacity > 64): the same
+// semantics, knn_insert one candidate at a time over 32-slot chunks.
+__global__ __launch_bounds__(256) void k_apply_wide(u64 n, u32 k, u32 S, u64* __restrict__ keys,
+                                                    u32* __restrict__ flags,
+                                                    float* __restrict__ worst,
+                                                    u64* __restrict__ slots,
+                                                    u64* __restrict__ counters,
+                                                    const float* __restrict__ X, int d) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  u64 acc_total = 0;
+  for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); p < n; p += warps) {
+    u64* sl = slots + p * S;
+    u64 rk = kEmptyKey, last = 0;
+    u32 fl = 0, from_c = 0;
     bool loaded = false;
-    u32 fl = 0, accepted = 0;
-    u64 last = 0;
     for (u32 c0 = 0; c0 < S; c0 += 32) {
       const u32 si = c0 + lane;
-      const u64 s = si < S ? sl[si] : kEmptyKey;
-      const bool filled = s != kEmptyKey;
+      u64 cc = si < S ? sl[si] : kEmptyKey;
+      const bool filled = cc != kEmptyKey;
       if (filled) sl[si] = kEmptyKey;  // CandidateBuffer::reset
-      unsigned mask = __ballot_sync(kFull, filled);
-      if (!mask) continue;
+      if (!__any_sync(kFull, filled)) continue;
       if (!loaded) {
         loaded = true;
         rk = lane < k ? keys[p * k + lane] : kEmptyKey;
-        fl = (flags[p] >> lane) & 1u;
-        last = __shfl_sync(kFull, rk, k - 1);
+        fl = lane < k ? (flags[p] >> lane) & 1u : 0u;
+        last = shfl64(rk, k - 1);
       }
-      u64 sx = s;
-      if (X && filled && s < last) {
-        const u32 v = key_id(s);
-        sx = pack_key(l2_exact(X + p * (u64)d, X + (u64)v * d, d), v);
+      if (X && filled && cc < last) {
+        const u32 v = key_id(cc);
+        cc = pack_key(l2_exact(X + p * (u64)d, X + (u64)v * d, d), v);
       }
-      mask = __ballot_sync(kFull, filled && sx < last);
+      unsigned mask = __ballot_sync(kFull, filled && cc < last);
       while (mask) {
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
-        const u64 c = __shfl_sync(kFull, sx, src);
-        // knn_insert core.cpp:99-112: reject duplicates and non-improvements
+        const u64 c = shfl64(cc, src);
         if (c >= last) continue;
         if (__ballot_sync(kFull, lane < k && key_id(rk) == key_id(c))) continue;
         const u32 pos = __popc(__ballot_sync(kFull, lane < k && rk < c));
         const u64 up = __shfl_up_sync(kFull, rk, 1);
-        const u32 upf = __shfl_up_sync(kFull, fl, 1);
+        const u32 upf = __shfl_up_sync(kFull, fl | (from_c << 1), 1);
         if (lane > pos && lane < k) {
           rk = up;
-          fl = upf;
+          fl = upf & 1u;
+          from_c = upf >> 1;
         }
         if (lane == pos) {
           rk = c;
           fl = 1;
+          from_c = 1;
         }
-        last = __shfl_sync(kFull, rk, k - 1);
-        ++accepted;
+        last = shfl64(rk, k - 1);
       }
     }
-    if (accepted) {
+    const u32 kept = __popc(__ballot_sync(kFull, lane < k && from_c));
+    if (kept) {
       if (lane < k) keys[p * k + lane] = rk;
       const unsigned fmask = __ballot_sync(kFull, fl && lane < k);
       if (lane == 0) {
         flags[p] = fmask;
         worst[p] = key_dist(last);
       }
-      acc_total += accepted;
+      acc_total += kept;
     }
   }
   if (lane == 0 && acc_total)
@@ -977,8 +1137,13 @@ void nn_descent_core(Runner& r, const DevRows& ds, const NndParams& p, uint64_t*
       tm.tick(kStOffer);
       launches += 2;
     }
-    k_apply<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst_p, slots_p,
-                                                   counters_p, use_tc ? ds.x : nullptr, ds.d);
+    if (S <= 64)
+      k_apply<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst_p, slots_p,
+                                                     counters_p, use_tc ? ds.x : nullptr, ds.d);
+    else
+      k_apply_wide<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst_p, slots_p,
+                                                          counters_p, use_tc ? ds.x : nullptr,
+                                                          ds.d);
     KNNG_LAUNCH_CHECK();
     launches += 1;
     tm.tick(kStApply);
