@@ -218,13 +218,30 @@ __device__ __forceinline__ bool joins(u32 t, const u32* __restrict__ nfn,
                                       const u32* __restrict__ cnt_new) {
   return nfn[t] > 0 || cnt_new[t] > 0;
 }
+// the same predicate as a bitmap (n bits: 1.25 MB at 10M points, L2-resident)
+// -- the prune's random lookups hit it instead of two n-entry arrays
+__device__ __forceinline__ bool joins_bit(u32 t, const u32* __restrict__ bits) {
+  return (__ldg(bits + (t >> 5)) >> (t & 31)) & 1u;
+}
+// warp per 32 points
+__global__ __launch_bounds__(256) void k_join_bits(u64 n, const u32* __restrict__ nfn,
+                                                   const u32* __restrict__ cnt_new,
+                                                   u32* __restrict__ bits) {
+  const unsigned lane = lane_id();
+  const u64 words = (n + 31) >> 5;
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 w = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); w < words; w += warps) {
+    const u64 t = w * 32 + lane;
+    const unsigned b = __ballot_sync(kFull, t < n && joins((u32)t, nfn, cnt_new));
+    if (lane == 0) bits[w] = b;
+  }
+}
 
 // warp per source: how many of its old entries survive the prune; counts
 // the surviving reverse entries per target
 __global__ __launch_bounds__(256) void k_old_count(u64 n, u32 k, const u32* __restrict__ of,
                                                    const u32* __restrict__ ofn,
-                                                   const u32* __restrict__ nfn,
-                                                   const u32* __restrict__ cnt_new,
+                                                   const u32* __restrict__ jbits,
                                                    u32* __restrict__ src_cnt,
                                                    u32* __restrict__ cnt_old) {
   const unsigned lane = lane_id();
@@ -233,7 +250,7 @@ __global__ __launch_bounds__(256) void k_old_count(u64 n, u32 k, const u32* __re
     bool keep = false;
     if (lane < ofn[p]) {
       const u32 t = of[p * k + lane];
-      keep = joins(t, nfn, cnt_new);
+      keep = joins_bit(t, jbits);
       if (keep) atomicAdd(&cnt_old[t], 1u);
     }
     const unsigned kb = __ballot_sync(kFull, keep);
@@ -245,8 +262,7 @@ __global__ __launch_bounds__(256) void k_old_count(u64 n, u32 k, const u32* __re
 __global__ __launch_bounds__(256) void k_emit_pairs(u64 n, u32 width, const u32* __restrict__ fwd,
                                                     const u32* __restrict__ cnt,
                                                     const u64* __restrict__ src_off,
-                                                    const u32* __restrict__ nfn,
-                                                    const u32* __restrict__ cnt_new,
+                                                    const u32* __restrict__ jbits,
                                                     u32* __restrict__ keys,
                                                     u32* __restrict__ vals) {
   const unsigned lane = lane_id();
@@ -256,7 +272,7 @@ __global__ __launch_bounds__(256) void k_emit_pairs(u64 n, u32 width, const u32*
     u32 t = 0;
     if (lane < cnt[p]) {
       t = fwd[p * width + lane];
-      keep = nfn == nullptr || joins(t, nfn, cnt_new);
+      keep = jbits == nullptr || joins_bit(t, jbits);
     }
     const unsigned kb = __ballot_sync(kFull, keep);
     if (keep) {
@@ -336,7 +352,7 @@ __global__ __launch_bounds__(256) void k_rev_scatter(u64 n, u32 k, u32 B, const 
                                                      const u32* __restrict__ nfn,
                                                      const u32* __restrict__ of,
                                                      const u32* __restrict__ ofn,
-                                                     const u32* __restrict__ cnt_new,
+                                                     const u32* __restrict__ jbits,
                                                      const u64* __restrict__ off_new,
                                                      const u64* __restrict__ off_old,
                                                      u32* __restrict__ cur_new,
@@ -357,7 +373,7 @@ __global__ __launch_bounds__(256) void k_rev_scatter(u64 n, u32 k, u32 B, const 
       rev_put(tn, on_n, (u32)p, off_new, cur_new, buf_new);
       bool on_o = j < co;
       const u32 to = on_o ? of[p * k + j] : 0;
-      on_o = on_o && joins(to, nfn, cnt_new);
+      on_o = on_o && joins_bit(to, jbits);
       rev_put(to, on_o, (u32)p, off_old, cur_old, buf_old);
     }
   }
@@ -875,8 +891,11 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
   KNNG_LAUNCH_CHECK();
   lap("zero+sample_fwd");
   if (prune_old) {
-    k_old_count<<<g, 256, 0, r.stream>>>(n, k, s.of.p, s.ofn.p, s.nfn.p, c.cnt_new.p,
-                                         c.src_cnt.p, c.cnt_old.p);
+    k_join_bits<<<warp_grid(r, (n + 31) / 32), 256, 0, r.stream>>>(n, s.nfn.p, c.cnt_new.p,
+                                                                    c.join_bits.p);
+    KNNG_LAUNCH_CHECK();
+    k_old_count<<<g, 256, 0, r.stream>>>(n, k, s.of.p, s.ofn.p, c.join_bits.p, c.src_cnt.p,
+                                         c.cnt_old.p);
     KNNG_LAUNCH_CHECK();
     exclusive_scan_u32(r, c.src_cnt.p, c.src_off_old.p, n);
   } else {
@@ -890,7 +909,7 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
     c.cur_new.zero();
     c.cur_old.zero();
     k_rev_scatter<<<g, 256, 0, r.stream>>>(n, k, B, s.nf.p, s.nfn.p, s.of.p, s.ofn.p,
-                                           c.cnt_new.p, c.off_new.p, c.off_old.p, c.cur_new.p,
+                                           c.join_bits.p, c.off_new.p, c.off_old.p, c.cur_new.p,
                                            c.cur_old.p, c.key_new.p, c.key_old.p);
     KNNG_LAUNCH_CHECK();
     c.long_cnt.zero();
@@ -902,19 +921,18 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
                                                            c.off_old.p, c.key_old.p, s.nr.p,
                                                            s.orv.p, c.long_cnt.p, c.long_rec.p);
     KNNG_LAUNCH_CHECK();
-    if (launches) *launches += 4 + 2 + 2 * 3 + 3;
+    if (launches) *launches += 4 + 3 + 2 * 3 + 3;
     return;
   }
   exclusive_scan_u32(r, s.nfn.p, c.src_off_new.p, n);
   exclusive_scan_u32(r, c.cnt_new.p, c.off_new.p, n);
   exclusive_scan_u32(r, c.cnt_old.p, c.off_old.p, n);
   lap("scans");
-  k_emit_pairs<<<g, 256, 0, r.stream>>>(n, B, s.nf.p, s.nfn.p, c.src_off_new.p, nullptr, nullptr,
+  k_emit_pairs<<<g, 256, 0, r.stream>>>(n, B, s.nf.p, s.nfn.p, c.src_off_new.p, nullptr,
                                         c.key_new.p, c.val_new.p);
   KNNG_LAUNCH_CHECK();
   k_emit_pairs<<<g, 256, 0, r.stream>>>(n, k, s.of.p, s.ofn.p, c.src_off_old.p,
-                                        prune_old ? s.nfn.p : nullptr,
-                                        prune_old ? c.cnt_new.p : nullptr, c.key_old.p,
+                                        prune_old ? c.join_bits.p : nullptr, c.key_old.p,
                                         c.val_old.p);
   KNNG_LAUNCH_CHECK();
   lap("emit");
@@ -930,7 +948,7 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
                                         c.off_old.p, to ? c.tv_old.p : c.val_old.p, s.nr.p,
                                         s.nrn.p, s.orv.p, s.orn.p);
   KNNG_LAUNCH_CHECK();
-  if (launches) *launches += 4 + (prune_old ? 2 : 1) + 4 * 3 + 2 * 9;
+  if (launches) *launches += 4 + (prune_old ? 3 : 1) + 4 * 3 + 2 * 9;
 }
 
 void alloc_lists(Runner& r, uint64_t n, uint32_t k, uint32_t B, SampleLists& s, RevCsr& c) {
@@ -946,6 +964,7 @@ void alloc_lists(Runner& r, uint64_t n, uint32_t k, uint32_t B, SampleLists& s, 
   s.orn.alloc(r, n);
   c.cnt_new.alloc(r, n);
   c.cnt_old.alloc(r, n);
+  c.join_bits.alloc(r, (n + 31) / 32 + 1);
   c.cur_new.alloc(r, n);
   c.cur_old.alloc(r, n);
   // hub segments (> kRankSmem entries): at most (new + old entries) / kRankSmem

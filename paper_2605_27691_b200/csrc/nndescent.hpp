@@ -79,6 +79,7 @@ struct SampleLists {
 // reverse-list scratch of one sampling pass (counts, offsets, pair buffers)
 struct RevCsr {
   DBuf<uint32_t> cnt_new, cnt_old, src_cnt, cur_new, cur_old, long_cnt, long_rec;
+  DBuf<uint32_t> join_bits;  // joins(t) per point (n bits), for the old-list prune
   DBuf<uint64_t> off_new, off_old, src_off_new, src_off_old;
   DBuf<uint32_t> key_new, val_new, key_old, val_old, tk_new, tv_new, tk_old, tv_old;
 };
