@@ -381,6 +381,50 @@ __global__ __launch_bounds__(256) void k_rev_scatter(u64 n, u32 k, u32 B, const 
 
 constexpr u32 kRankSmem = 512;  // per-warp smem rank sort capacity
 
+// Ascending bitonic sort of 32 R keys held R per lane (element j*32 + lane in
+// v[j]); strides >= 32 compare registers of one lane, shorter ones shuffle.
+template <int R>
+__device__ __forceinline__ void warp_sort_regs(u32 (&v)[R], unsigned lane) {
+#pragma unroll
+  for (unsigned size = 2; size <= 32u * R; size <<= 1)
+#pragma unroll
+    for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+        const unsigned js = stride >> 5;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          if (j & js) continue;
+          const unsigned e = (unsigned)j * 32 + lane;
+          const bool up = (e & size) == 0;
+          const u32 a = v[j], b = v[j ^ js];
+          if ((a > b) == up) {
+            v[j] = b;
+            v[j ^ js] = a;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const unsigned e = (unsigned)j * 32 + lane;
+          const u32 o = __shfl_xor_sync(kFull, v[j], stride);
+          const bool keep_min = ((lane & stride) == 0) == ((e & size) == 0);
+          v[j] = keep_min ? min(v[j], o) : max(v[j], o);
+        }
+      }
+    }
+}
+// pick the element of rank r (all lanes take part; r < 32 R)
+template <int R>
+__device__ __forceinline__ u32 warp_pick_regs(const u32 (&v)[R], u32 r) {
+  u32 out = 0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const u32 x = __shfl_sync(kFull, v[j], r & 31);
+    if ((r >> 5) == (u32)j) out = x;
+  }
+  return out;
+}
+
 __global__ __launch_bounds__(256) void k_rev_select_rank(u64 n, u32 B, u64 iter_seed,
                                                          const u64* __restrict__ off_new,
                                                          const u32* __restrict__ buf_new,
@@ -420,6 +464,20 @@ __global__ __launch_bounds__(256) void k_rev_select_rank(u64 n, u32 B, u64 iter_
         const u64 x = lane < len ? (u64)seg[lane] : ~0ull;
         const u32 sorted = (u32)warp_sort32(x);
         const u32 pick = __shfl_sync(kFull, sorted, lane < B ? sp[lane] : 0);
+        if (lane < B) out[lane] = pick;
+      } else if (len <= 64) {
+        u32 v[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) v[j] = j * 32 + lane < len ? seg[j * 32 + lane] : 0xffffffffu;
+        warp_sort_regs<2>(v, lane);
+        const u32 pick = warp_pick_regs<2>(v, lane < B ? sp[lane] : 0);
+        if (lane < B) out[lane] = pick;
+      } else if (len <= 128) {
+        u32 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = j * 32 + lane < len ? seg[j * 32 + lane] : 0xffffffffu;
+        warp_sort_regs<4>(v, lane);
+        const u32 pick = warp_pick_regs<4>(v, lane < B ? sp[lane] : 0);
         if (lane < B) out[lane] = pick;
       } else if (len <= kRankSmem) {
         // bitonic sort of the segment (padded to a power of two) in smem
@@ -859,16 +917,19 @@ namespace {
 
 
 // Which reverse-list path nn_descent takes (both give bit-identical graphs,
-// tests/test_parity_gpu.py).  The scatter path is random-access bound: it wins
-// while its per-target cursor/offset arrays stay L2-resident (C2 1M points:
-// sampling 24.9 -> 21.6 ms per build) and loses to the radix sort's streaming
-// passes beyond (C4 10M points: 2.24 -> 2.65 s; profiles/r02_sampling_paths.md),
-// so it is used up to 2M points.  KNNG_REV_SORT=1 / =0 forces either path.
+// tests/test_parity_gpu.py): the scatter path unless KNNG_REV_SORT=1.  With
+// segments of <= 32 ranked by a warp sort and 33-512 in shared memory it won
+// at 1M points (sampling 24.9 -> 21.6 ms per build) and lost at 10M
+// (2.24 -> 2.65 s; profiles/r02_sampling_paths.md); ranking 33-128 in
+// registers (warp_sort_regs) and the joins bitmap turned that around.
 bool rev_sort_forced(uint64_t n) {
   const char* v = std::getenv("KNNG_REV_SORT");
   if (v && v[0] == '1') return true;
-  if (v && v[0] == '0') return false;
-  return n > (2ull << 20);
+  (void)n;
+  // the scatter path at every size since its segments of 33-128 entries are
+  // ranked in registers: 10M x 96 clustered(16) builds 3.86 s vs 4.13 s
+  // sorted, 5M 1.51 vs 1.57 s (round 2; before, the sort won beyond 2M)
+  return false;
 }
 
 void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_seed,

@@ -10,7 +10,8 @@ x = torch.from_numpy(knng.gen_random_dataset(n, d, "clustered", 42, cl)).cuda()
 for _ in range(reps):
     st = knng.NnDescentStats()
     torch.cuda.synchronize(); t = time.perf_counter()
-    g = knng.nn_descent(x, knng.NnDescentParams(k=32, seed=1), stats=st)
+    g = knng.nn_descent(x, knng.NnDescentParams(k=32, seed=1),
+                        stats=None if os.environ.get("NOSTATS") else st)
     torch.cuda.synchronize()
     print(dict(env={k: v for k, v in os.environ.items() if k.startswith("KNNG_")}, n=n, d=d,
                secs=round(time.perf_counter() - t, 3), iters=st.iterations,
