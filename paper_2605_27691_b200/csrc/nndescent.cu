@@ -522,9 +522,18 @@ __global__ __launch_bounds__(256) void k_rev_select_rank(u64 n, u32 B, u64 iter_
 }
 
 // Hub segments (longer than kRankSmem): one CTA each selects the elements of
-// the B sampled ranks by radix select over the segment in global memory --
-// four 8-bit passes; after them each rank's prefix IS its element (sources
-// in a segment are distinct).  O(len) per segment, however long.
+// the B sampled ranks by radix select -- 8-bit digits from the top bits that
+// vary; after the last pass each rank's prefix IS its element (sources in a
+// segment are distinct).  O(len) per pass:
+//   * ranks whose prefixes agree so far form a group with one histogram; the
+//     element -> group map of the next pass is a (group, digit) table, and a
+//     segment of <= kLongCache entries is kept in shared memory with its
+//     group byte, so an element costs a few shared-memory operations per
+//     pass (longer ones re-read HBM and match the <= B group prefixes);
+//   * each rank finds its bin by a warp scan of its group's 256 bins.
+constexpr u32 kLongCache = 8192;
+constexpr size_t kLongSmem = 32 * 256 * 4 + kLongCache * 4 + kLongCache + 32 * 256;
+
 __global__ __launch_bounds__(256) void k_rev_select_long(u64 n_src, u32 B,
                                                          const u64* __restrict__ off_new,
                                                          const u32* __restrict__ buf_new,
@@ -534,11 +543,15 @@ __global__ __launch_bounds__(256) void k_rev_select_long(u64 n_src, u32 B,
                                                          u32* __restrict__ orv,
                                                          const u32* __restrict__ long_cnt,
                                                          const u32* __restrict__ long_rec) {
-  __shared__ u32 hist[32][256];
-  __shared__ u32 prefix[32], remain[32], lead[32];
+  extern __shared__ __align__(16) unsigned char smem_long[];
+  u32* hist = reinterpret_cast<u32*>(smem_long);              // [32][256]
+  u32* xs = hist + 32 * 256;                                   // [kLongCache]
+  unsigned char* grp = reinterpret_cast<unsigned char*>(xs + kLongCache);  // [kLongCache]
+  unsigned char* child = grp + kLongCache;                     // [32][256]
+  __shared__ u32 prefix[32], remain[32], gid[32], gpre[32], bin_of[32];
+  __shared__ int G;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const u32 nrec = *long_cnt;
-  // source ids are < n: digits start at the top bits that vary (a first digit
-  // of all-zero high bits would pile every element onto one histogram bin)
   int top = 0;
   while (top < 32 && (n_src >> top) > 0) ++top;
   const int first_shift = top > 8 ? ((top - 8 + 7) / 8) * 8 : 0;
@@ -549,46 +562,104 @@ __global__ __launch_bounds__(256) void k_rev_select_long(u64 n_src, u32 B,
     const u64* off = which ? off_old : off_new;
     const u32* seg = (which ? buf_old : buf_new) + off[v];
     const u32 len = (u32)(off[v + 1] - off[v]);
+    const bool cached = len <= kLongCache;
+    if (cached)
+      for (u32 i = threadIdx.x; i < len; i += blockDim.x) {
+        xs[i] = seg[i];
+        grp[i] = 0;
+      }
     if (threadIdx.x < B) {
       prefix[threadIdx.x] = 0;
       remain[threadIdx.x] = rec[2 + threadIdx.x];
+      gid[threadIdx.x] = 0;
     }
+    if (threadIdx.x == 0) {
+      G = 1;
+      gpre[0] = 0;
+    }
+    __syncthreads();
+    int prev_shift = -1;  // the digit that indexes `child` (previous pass)
     for (int shift = first_shift; shift >= 0; shift -= 8) {
-      for (u32 i = threadIdx.x; i < B * 256; i += blockDim.x) hist[i >> 8][i & 255] = 0;
+      const int g_n = G;
+      for (u32 i = threadIdx.x; i < (u32)g_n * 256; i += blockDim.x) hist[i] = 0;
       __syncthreads();
       const u32 hi_mask = shift >= 24 ? 0u : (0xffffffffu << (shift + 8));
-      // ranks sharing the bits decided so far share one histogram (its leader)
-      if (threadIdx.x < B) {
-        u32 l = threadIdx.x;
-        for (u32 b = 0; b < threadIdx.x; ++b)
-          if ((prefix[b] & hi_mask) == (prefix[threadIdx.x] & hi_mask)) {
-            l = b;
-            break;
-          }
-        lead[threadIdx.x] = l;
-      }
-      __syncthreads();
       for (u32 i = threadIdx.x; i < len; i += blockDim.x) {
-        const u32 x = seg[i];
-        for (u32 b = 0; b < B; ++b)
-          if (lead[b] == b && (x & hi_mask) == (prefix[b] & hi_mask)) {
-            atomicAdd(&hist[b][(x >> shift) & 255], 1u);
-            break;  // the groups' prefixes are disjoint
+        u32 x, g;
+        if (cached) {
+          // the element's group moves by the previous pass's (group, digit)
+          x = xs[i];
+          g = grp[i];
+          if (prev_shift >= 0 && g != 0xff) {
+            g = child[g * 256 + ((x >> prev_shift) & 255)];
+            grp[i] = (unsigned char)g;
           }
+        } else {
+          x = seg[i];
+          g = 0xff;
+          for (int b = 0; b < g_n; ++b)
+            if ((x & hi_mask) == (gpre[b] & hi_mask)) {
+              g = b;
+              break;
+            }
+        }
+        if (g != 0xff) atomicAdd(&hist[g * 256 + ((x >> shift) & 255)], 1u);
       }
       __syncthreads();
-      if (threadIdx.x < B) {
-        const u32 b = threadIdx.x;
-        const u32 hb = lead[b];
-        u32 acc = 0, bin = 0;
-        for (; bin < 256; ++bin) {
-          const u32 h = hist[hb][bin];
-          if (acc + h > remain[b]) break;
-          acc += h;
+      // rank r (warp r % 8): lane l scans bins 8l..8l+7 of the rank's group
+      for (u32 r = warp; r < B; r += blockDim.x >> 5) {
+        const u32* h = hist + gid[r] * 256 + lane * 8;
+        u32 c[8], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          c[j] = h[j];
+          tot += c[j];
         }
-        prefix[b] |= bin << shift;
-        remain[b] -= acc;
+        u32 incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const u32 t = __shfl_up_sync(kFull, incl, o);
+          if ((int)lane >= o) incl += t;
+        }
+        const u32 excl = incl - tot, want = remain[r];
+        // the lane whose range holds rank `want`
+        const unsigned hit = __ballot_sync(kFull, excl <= want && want < incl);
+        if ((int)lane == __ffs(hit) - 1) {
+          u32 acc = excl, bin = lane * 8;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (acc + c[j] > want) break;
+            acc += c[j];
+            ++bin;
+          }
+          bin_of[r] = bin;
+          prefix[r] |= bin << shift;
+          remain[r] = want - acc;
+        }
       }
+      __syncthreads();
+      if (shift == 0) break;
+      // next groups (warp 0, lane = rank): ranks with the same (group, bin)
+      // share one; `child` maps an element's (group, digit) to it
+      if (warp == 0) {
+        const bool live = lane < B;
+        const u32 key = live ? gid[lane] * 256 + bin_of[lane] : 0xffffffffu;
+        const unsigned same = __match_any_sync(kFull, key);
+        const int leader = __ffs(same) - 1;
+        const unsigned leaders = __ballot_sync(kFull, live && leader == (int)lane);
+        const u32 ng = __popc(leaders & ((1u << leader) - 1u));
+        // clear this pass's table rows, then the leaders write theirs
+        for (u32 i = lane; i < (u32)g_n * 64; i += 32)
+          reinterpret_cast<u32*>(child)[i] = 0xffffffffu;
+        __syncwarp();
+        if (live && leader == (int)lane) {
+          child[key] = (unsigned char)ng;
+          gpre[ng] = prefix[lane];
+        }
+        if (live) gid[lane] = ng;
+        if (lane == 0) G = __popc(leaders);
+      }
+      prev_shift = shift;
       __syncthreads();
     }
     if (threadIdx.x < B) (which ? orv : nr)[v * B + threadIdx.x] = prefix[threadIdx.x];
@@ -978,7 +1049,10 @@ void sample_into(Runner& r, uint64_t n, uint32_t k, uint32_t B, uint64_t iter_se
                                                c.off_old.p, c.key_old.p, s.nr.p, s.nrn.p,
                                                s.orv.p, s.orn.p, c.long_cnt.p, c.long_rec.p);
     KNNG_LAUNCH_CHECK();
-    k_rev_select_long<<<r.num_sms * 2, 256, 0, r.stream>>>(n, B, c.off_new.p, c.key_new.p,
+    // (idempotent; cheap next to the sampling launches)
+    KNNG_CUDA(cudaFuncSetAttribute(k_rev_select_long,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLongSmem));
+    k_rev_select_long<<<r.num_sms * 2, 256, kLongSmem, r.stream>>>(n, B, c.off_new.p, c.key_new.p,
                                                            c.off_old.p, c.key_old.p, s.nr.p,
                                                            s.orv.p, c.long_cnt.p, c.long_rec.p);
     KNNG_LAUNCH_CHECK();
