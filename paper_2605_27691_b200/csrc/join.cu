@@ -143,7 +143,8 @@ __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
                                                u32 chunks, u64* __restrict__ slots, u32 S,
                                                u32 nb, u32 ways, u64* __restrict__ counters,
                                                u64 p_lo, const u64* __restrict__ n_live,
-                                               u32 t_lo, u32 t_hi) {
+                                               u32 t_lo, u32 t_hi,
+                                               uint8_t* __restrict__ touched) {
   if (n_live) {  // the slice's live chunk count, read on the device
     const u64 live = *n_live;
     const u64 hi = live < p_lo ? 0 : live - p_lo;
@@ -162,12 +163,14 @@ __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
       u64 key[kOfferBatch];
       u64* bk[kOfferBatch];
       u32 pos[kOfferBatch];
+      u32 key_tgt[kOfferBatch];
 #pragma unroll
       for (int i = 0; i < kOfferBatch; ++i) {
         const u32 e = e0 + i * blockDim.x;
         bk[i] = nullptr;
         if (e < fill) {
           const u32 tgt = q_tgt[base + e];
+          key_tgt[i] = tgt;
           if (tgt >= t_lo && tgt < t_hi) {
             key[i] = q_key[base + e];
             bk[i] = slots + (u64)tgt * S + (u64)bucket_hash(tgt, key_id(key[i]), nb) * ways;
@@ -200,6 +203,8 @@ __global__ __launch_bounds__(256) void k_offer(const u64* __restrict__ q_key,
           p += (w < ways && sn[w] < key[i]) ? 1u : 0u;
         }
         pos[i] = (dup || p >= ways) ? 4u : p;
+        // the target's buffer may change: k_apply visits touched points only
+        if (touched && pos[i] < ways) touched[key_tgt[i]] = 1;
       }
       // rounds: one independent atomicMin per live offer (pipelined), then
       // carry the larger of (old, key) to the next slot (the cascade above)
@@ -1017,7 +1022,8 @@ void launch_join(const Runner& r, const JoinPlan& plan, const JoinLaunch& l) {
 void launch_offer(const Runner& r, const JoinPlan& plan, const uint64_t* q_key,
                   const uint32_t* q_tgt, const uint32_t* q_fill, uint32_t chunks,
                   uint64_t* slots, uint32_t S, uint32_t nb, uint32_t ways, uint64_t* counters,
-                  uint64_t p_lo, const uint64_t* n_live, uint64_t n_points) {
+                  uint64_t p_lo, const uint64_t* n_live, uint64_t n_points,
+                  uint8_t* touched) {
   if (!chunks) return;
   const unsigned grid = (unsigned)std::min<uint64_t>(chunks, (uint64_t)r.num_sms * 8);
   // one pass by default: target-range passes with L2-resident bucket rows
@@ -1032,7 +1038,7 @@ void launch_offer(const Runner& r, const JoinPlan& plan, const uint64_t* q_key,
     const u32 hi = (u32)std::min<uint64_t>((b + 1) * per, n_points);
     k_offer<<<grid, 256, 0, r.stream>>>(q_key, q_tgt, q_fill, plan.q_per_chunk, chunks, slots,
                                         S, nb, ways, counters, p_lo, n_live, lo,
-                                        passes == 1 ? 0xffffffffu : hi);
+                                        passes == 1 ? 0xffffffffu : hi, touched);
     KNNG_LAUNCH_CHECK();
   }
 }

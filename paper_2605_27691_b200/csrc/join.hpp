@@ -70,6 +70,7 @@ void launch_offer(const Runner& r, const JoinPlan& plan, const uint64_t* q_key,
                   const uint32_t* q_tgt, const uint32_t* q_fill, uint32_t chunks,
                   uint64_t* slots, uint32_t S, uint32_t nb, uint32_t ways,
                   uint64_t* counters = nullptr, uint64_t p_lo = 0,
-                  const uint64_t* n_live = nullptr, uint64_t n_points = 0);
+                  const uint64_t* n_live = nullptr, uint64_t n_points = 0,
+                  uint8_t* touched = nullptr);
 
 }  // namespace knng_b200

@@ -716,16 +716,29 @@ __device__ __forceinline__ u64 warp_merge_asc(u64 v, unsigned lane) {
 
 constexpr u32 kApplySerialMax = 8;  // candidates up to which knn_insert runs one by one
 
+// Only points an offer reached (touched, set by k_offer) can hold candidates:
+// a warp takes 32 points, reads their touched bytes at once and visits the
+// set ones.  Used once offers get sparse (the iteration before queued fewer
+// than 4 per point); with touched null every point is visited (k_offer then
+// writes no flags -- early iterations reach almost every point anyway).
 __global__ __launch_bounds__(256) void k_apply(u64 n, u32 k, u32 S, u64* __restrict__ keys,
                                                u32* __restrict__ flags,
                                                float* __restrict__ worst,
                                                u64* __restrict__ slots,
                                                u64* __restrict__ counters,
-                                               const float* __restrict__ X, int d) {
+                                               const float* __restrict__ X, int d,
+                                               uint8_t* __restrict__ touched) {
   const unsigned lane = lane_id();
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
   u64 acc_total = 0;
-  for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); p < n; p += warps) {
+  for (u64 p0 = ((((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * 32; p0 < n;
+       p0 += warps * 32) {
+   const bool mine = p0 + lane < n && (!touched || touched[p0 + lane]);
+   if (mine && touched) touched[p0 + lane] = 0;
+   unsigned todo = __ballot_sync(kFull, mine);
+   while (todo) {
+    const u64 p = p0 + (__ffs(todo) - 1);
+    todo &= todo - 1;
     u64* sl = slots + p * S;
     // the buffer (S <= 64: two keys per lane), reset as it is read
     u64 c[2];
@@ -830,6 +843,7 @@ __global__ __launch_bounds__(256) void k_apply(u64 n, u32 k, u32 S, u64* __restr
       }
       acc_total += kept;
     }
+   }
   }
   if (lane == 0 && acc_total)
     atomicAdd(reinterpret_cast<unsigned long long*>(counters + kCntAccepted), acc_total);
@@ -1166,6 +1180,8 @@ void nn_descent_core(Runner& r, const DevRows& ds, const NndParams& p, uint64_t*
   float* worst_p = ws_buf(r, &W.worst, W.worst, n);
   u64* slots_p = ws_buf(r, &W.slots, W.slots, n * S);
   KNNG_CUDA(cudaMemsetAsync(slots_p, 0xff, n * S * sizeof(u64), r.stream));
+  uint8_t* touched_p = ws_buf(r, &W.touched, W.touched, n);
+  KNNG_CUDA(cudaMemsetAsync(touched_p, 0, n, r.stream));
   u64* counters_p = ws_buf(r, &W.counters, W.counters, kNumCounters);
   auto zero_counters = [&] {
     KNNG_CUDA(cudaMemsetAsync(counters_p, 0, kNumCounters * sizeof(u64), r.stream));
@@ -1257,7 +1273,9 @@ void nn_descent_core(Runner& r, const DevRows& ds, const NndParams& p, uint64_t*
     cudaEvent_t e;
     ~EvGuard() { cudaEventDestroy(e); }
   } iter_done_guard{iter_done};
+  u64 prev_offers = ~0ull;  // offers queued by the previous iteration
   for (u64 iter = 0; iter < p.max_iters; ++iter) {
+    const bool use_touched = S <= 64 && prev_offers < 4 * n;
     zero_counters();
     const u64 iter_seed = mix_seed(p.seed, 0x5a3f1e00ull + iter);
     sample_into(r, n, k, B, iter_seed, keys, flags, s, c, true, &launches);
@@ -1287,13 +1305,14 @@ void nn_descent_core(Runner& r, const DevRows& ds, const NndParams& p, uint64_t*
       tm.tick(kStJoin);
       launch_offer(r, plan, q_key_p, q_tgt_p, q_fill_p,
                    (u32)ceil_div<u64>(jl.p_hi - jl.p_lo, (u64)kJoinChunk), slots_p, S, nb, ways,
-                   counters_p, jl.p_lo, jl.n_live, n);
+                   counters_p, jl.p_lo, jl.n_live, n, use_touched ? touched_p : nullptr);
       tm.tick(kStOffer);
       launches += 2;
     }
     if (S <= 64)
-      k_apply<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst_p, slots_p,
-                                                     counters_p, use_tc ? ds.x : nullptr, ds.d);
+      k_apply<<<warp_grid(r, (n + 31) / 32), 256, 0, r.stream>>>(
+          n, k, S, keys, flags, worst_p, slots_p, counters_p, use_tc ? ds.x : nullptr, ds.d,
+          use_touched ? touched_p : nullptr);
     else
       k_apply_wide<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, keys, flags, worst_p, slots_p,
                                                           counters_p, use_tc ? ds.x : nullptr,
@@ -1312,6 +1331,7 @@ void nn_descent_core(Runner& r, const DevRows& ds, const NndParams& p, uint64_t*
     KNNG_CUDA(cudaGetLastError());
     tm.tick(kStSync);
     const u64 accepted = hcount.p[kCntAccepted];
+    prev_offers = hcount.p[kCntOffers];
     if (std::getenv("KNNG_TRACE"))
       std::fprintf(stderr, "[knng nnd] dev %d t %.1f ms iter %llu pairs %llu offers %llu seen %llu accepted %llu\n",
                    r.device,

@@ -94,6 +94,7 @@ struct NndWorkspace {
   uint64_t lists_n = 0;
   uint32_t lists_k = 0, lists_b = 0;
   DBuf<float> worst;
+  DBuf<uint8_t> touched;  // points an offer reached this iteration (k_offer -> k_apply)
   DBuf<uint64_t> counters, act_off;
   DBuf<uint32_t> L_cnt, act, act_flag, q_fill, chunk_ctr;
   uint64_t q_chunks_per_slice = 0;  // offer-queue slicing decided once per shape
