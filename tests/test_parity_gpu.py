@@ -433,7 +433,10 @@ def _sample(n):
                                   "c4r_100k_d96_clustered16_p4", "c4r_100k_d96_clustered16_p8",
                                   # BASELINE configs[1..3] at full size
                                   "c2_1m_clustered1000_k32", "c3_1m_d960_clustered1000_k32",
-                                  "c4_10m_d96_clustered16_p2", "c4_10m_d96_clustered16_p4"])
+                                  "c4_10m_d96_clustered16_p2", "c4_10m_d96_clustered16_p4",
+                                  # C4's shape at 2M points (the reference at 10M does
+                                  # not fit the container's host RAM)
+                                  "c4m_2m_d96_clustered16_p2", "c4m_2m_d96_clustered16_p4"])
 def test_recall_parity_vs_reference(knng, name):
     ref = _ref_recall().get(name)
     if ref is None:
@@ -452,6 +455,7 @@ def test_recall_parity_vs_reference(knng, name):
     rows = _sample(ref["n"])
     gt, _ = knng.brute_force_knng(x, 10, rows=rows)
     mine = recall(ids[rows.astype(np.int64)], gt)
+    print("recall parity", name, "b200", mine, "reference", ref["recall_at_10"])
     assert mine >= ref["recall_at_10"] - 0.005, (mine, ref["recall_at_10"])
 
 
