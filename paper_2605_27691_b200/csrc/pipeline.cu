@@ -177,13 +177,16 @@ void tree_level(Shared& S, RankState& R, uint64_t level, DBuf<float>& span_x, ui
     pull_rows(S, R, j, kDataset, px.p + at * S.d);
     pull_rows(S, R, j, kGraph, pk.p + at * S.k);
   }
+  trace_synced(R, "tree pulled");
   DBuf<u32> sg(r, cnt * S.od);
   {
     const DBuf<float> pn = norms_of(S, r, px.p, cnt);
     optimize_graph_device(r, pk.p, cnt, (u32)S.k, (u32)base, px.p, S.d, (u32)S.od, sg.p, nullptr,
                           pn.p);
   }
+  trace_synced(R, "tree optimized");
   search_and_merge(S, R, sg.p, px.p, cnt, base);
+  trace_synced(R, "tree merged");
   // accumulate the span dataset in rank order (refine.cpp:216-226)
   DBuf<float> ns(r, (span_n + cnt) * S.d);
   const size_t row = (size_t)S.d * 4;
@@ -201,6 +204,7 @@ void tree_level(Shared& S, RankState& R, uint64_t level, DBuf<float>& span_x, ui
   span_x = std::move(ns);
   S.world->publish(R.rank, kGraph, R.keys.p, R.n_local * S.k * 8,
                    wire_region_size(RegionKind::knng, R.n_local, S.k), r);
+  trace_synced(R, "tree published");
   S.world->barrier(R.rank, r);
 }
 

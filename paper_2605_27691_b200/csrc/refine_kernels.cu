@@ -242,7 +242,16 @@ void partition_device(Runner& r, uint64_t n, uint32_t ranks, uint64_t seed, uint
   u64 pending = n - 1;
   u32* cur = pa.p;
   u32* nxt = pb.p;
-  unsigned long long h = 0;
+  // each round's pending count comes back through pinned memory, polled on
+  // an event (a pageable copy + sleeping stream sync per round stalled the
+  // host by up to ~0.7 s now and then with four ranks per box)
+  HBuf<unsigned long long> hc(1);
+  cudaEvent_t done;
+  KNNG_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t e;
+    ~EvGuard() { cudaEventDestroy(e); }
+  } done_guard{done};
   while (pending) {
     ++rounds;
     cnt.zero();
@@ -254,9 +263,13 @@ void partition_device(Runner& r, uint64_t n, uint32_t ranks, uint64_t seed, uint
     KNNG_LAUNCH_CHECK();
     k_shuffle_reset<<<g, 256, 0, r.stream>>>(cur, pending, jd.p, res.p, n);
     KNNG_LAUNCH_CHECK();
-    KNNG_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, r.stream));
-    r.sync();
-    pending = h;
+    KNNG_CUDA(cudaMemcpyAsync(hc.p, cnt.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                              r.stream));
+    KNNG_CUDA(cudaEventRecord(done, r.stream));
+    while (cudaEventQuery(done) == cudaErrorNotReady) {
+    }
+    KNNG_CUDA(cudaGetLastError());
+    pending = hc.p[0];
     std::swap(cur, nxt);
   }
   if (rounds_out) *rounds_out = rounds;
