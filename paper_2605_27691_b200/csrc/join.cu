@@ -626,6 +626,23 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
   Tile T[kTPT];
   float acc[kTPT][4][4];
   while (true) {
+    // One barrier per unit: after it the current unit's rows have landed
+    // (every thread waited for its own copies) and everyone is done with the
+    // previous unit -- its buffer, and at a batch change its desc slot.  The
+    // next unit's rows are then issued into that buffer while this one is
+    // computed.
+    cp_async_wait<0>();
+    __syncthreads();
+    if (pend_chunk >= 0) {
+      // the chunk's offers are all queued (slot pend_m is reloaded only two
+      // chunks later: its counter is final)
+      if (tid == 0) {
+        const u32 f = (u32)s.mhdr(pend_m)[2];
+        a.q_fill[pend_chunk] = f;
+        my_offers += f;
+      }
+      pend_chunk = -1;
+    }
     // ---- next unit: next dim chunk of this batch, next batch, or next chunk
     int nq = cq, nc0 = cc0 + a.DC, nbuf = cbuf ^ 1;
     bool have_next = true;
@@ -647,13 +664,7 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
         __syncthreads();
       }
     }
-    if (have_next) {
-      issue_rows<kPair>(a, s, nq, nc0, nbuf);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();  // current buffer landed for everyone
+    if (have_next) issue_rows<kPair>(a, s, nq, nc0, nbuf);
 
     // ---- compute the current unit
     const int m = s.dhdr(cq)[0];
@@ -861,16 +872,6 @@ __global__ __launch_bounds__(kJT, kJCtas) void k_join(JoinArgs a) {
       }
     }
     if (!have_next) break;
-    __syncthreads();  // everyone is done with buffer cbuf / desc slot before reuse
-    if (pend_chunk >= 0) {
-      // slot pend_m is reloaded only two chunks later: its counter is final
-      if (tid == 0) {
-        const u32 f = (u32)s.mhdr(pend_m)[2];
-        a.q_fill[pend_chunk] = f;
-        my_offers += f;
-      }
-      pend_chunk = -1;
-    }
     cq = nq;
     cc0 = nc0;
     cbuf = nbuf;
