@@ -311,16 +311,41 @@ __device__ __forceinline__ void beam_merge(u64 c, u64* __restrict__ beam,
     }
     keep = !(clo < bs && beam[clo] == c);
   }
-  const unsigned kb = __ballot_sync(kFull, keep);
+  unsigned kb = __ballot_sync(kFull, keep);
   if (!kb) return;
   const u32 nc = __popc(kb);
   // rank among the kept candidates (keys are distinct)
   u32 crank = 0;
-  for (unsigned m = kb; m;) {
-    const int j = __ffs(m) - 1;
-    m &= m - 1;
-    const u64 cj = __shfl_sync(kFull, c, j);
-    crank += (keep && cj < c) ? 1u : 0u;
+  if (nc > 8) {
+    // many: a bitonic sort of the kept keys (clo travels with its key) puts
+    // candidate of rank r on lane r -- 15 exchange steps instead of nc
+    // broadcast-compare rounds
+    u64 v = keep ? c : kEmptyKey;
+    u32 pl = clo;
+#pragma unroll
+    for (unsigned size = 2; size <= 32; size <<= 1)
+#pragma unroll
+      for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+        const u64 o = __shfl_xor_sync(kFull, v, stride);
+        const u32 op = __shfl_xor_sync(kFull, pl, stride);
+        const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
+        if (keep_min ? (o < v) : (o > v)) {
+          v = o;
+          pl = op;
+        }
+      }
+    keep = lane < nc;
+    c = v;
+    clo = pl;
+    crank = lane;
+    kb = __ballot_sync(kFull, keep);
+  } else {
+    for (unsigned m = kb; m;) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const u64 cj = __shfl_sync(kFull, c, j);
+      crank += (keep && cj < c) ? 1u : 0u;
+    }
   }
   if (keep) s_clo[__popc(kb & lanemask_lt())] = clo;
   // entries before the first insertion point keep their slots
