@@ -1,12 +1,12 @@
-"""Per-launch DRAM traffic of k_join from an ncu --metrics csv log (all launches of
-one build): writes profiles/join_traffic.json for bench.py's roofline.traffic.
-usage: join_traffic.py <ncu.csv> <capture description> [iterations]
+"""DRAM traffic of k_join from an ncu --metrics csv log: writes
+profiles/join_traffic.json for bench.py's roofline.traffic.
+usage: join_traffic.py <ncu.csv> <capture description>
 
-With [iterations] given, the captured launches are one whole build: under ncu's
-replay (memory save/restore) the offer-queue budget shrinks and every
-NN-Descent iteration runs as two slices, so traffic and time are summed over
-the build and divided by its iteration count -- the per-launch figure of the
-unsliced bench (one join launch per iteration)."""
+Only k_join launches count (the kernel name "k_join<...>": not k_join_lists /
+k_join_bits).  Under ncu's replay (memory save/restore) the offer-queue
+budget can shrink and an iteration then runs as two slices, so the file
+records DRAM bytes per millisecond of join time; bench.py multiplies it by
+its own measured time per (unsliced) launch."""
 import csv, json, os, sys
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 5]
 h = rows[0]
@@ -16,12 +16,12 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1, "us": 1e-
          "msecond": 1, "usecond": 1e-3, "nsecond": 1e-6}
 per = {}
 for r in rows[1:]:
-    if "k_join" not in r[ik]:
+    if "k_join<" not in r[ik]:
         continue
     d = per.setdefault(r[iid], {})
     d[r[im]] = float(r[iv].replace(",", "")) * scale.get(r[iu], 1)
 L = list(per.values())
-div = int(sys.argv[3]) if len(sys.argv) > 3 else len(L)
+div = len(L)
 rd = sum(d["dram__bytes_read.sum"] for d in L) / div
 wr = sum(d["dram__bytes_write.sum"] for d in L) / div
 ms = sum(d["gpu__time_duration.sum"] for d in L) / div
@@ -30,8 +30,7 @@ out = {"kernel": "k_join", "launches": len(L), "per": div, "capture": sys.argv[2
        "duration_ms": ms, "per_launch": [{"read": d["dram__bytes_read.sum"],
                                           "write": d["dram__bytes_write.sum"],
                                           "ms": d["gpu__time_duration.sum"]} for d in L],
-       "traffic_bytes_per_launch": rd + wr,
-       "summary": sys.argv[4] if len(sys.argv) > 4 else None}
+       "dram_bytes_per_ms": (rd + wr) / ms}
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 json.dump(out, open(os.path.join(root, "profiles", "join_traffic.json"), "w"), indent=1)
 print(json.dumps({k: v for k, v in out.items() if k != "per_launch"}))
