@@ -835,10 +835,16 @@ uint64_t build_distributed_rank(int device, size_t rank, size_t ranks, const Hos
   const float* Xd = X;
   if (!x_on_device) {
     // A rank needs only its own block (remote rows arrive over NVLink from
-    // their owners): from pinned host memory it gathers those rows directly
-    // (zero-copy over PCIe, 1/P of the dataset); pageable memory is copied.
+    // their owners), but its rows are a random 1/P of the dataset: gathering
+    // them zero-copy over PCIe (KNNG_ZEROCOPY=1, pinned memory only) made
+    // many small random reads -- C4 N = 2 e2e 3.80 s per step vs 2.81 s with
+    // one bulk copy of the whole dataset and a gather on the device (the
+    // default).
     void* mapped = nullptr;
-    if (cudaHostGetDevicePointer(&mapped, const_cast<float*>(X), 0) == cudaSuccess && mapped) {
+    const char* zc = std::getenv("KNNG_ZEROCOPY");
+    const bool zero_copy = zc && *zc && std::atoi(zc) != 0;
+    if (zero_copy &&
+        cudaHostGetDevicePointer(&mapped, const_cast<float*>(X), 0) == cudaSuccess && mapped) {
       Xd = static_cast<const float*>(mapped);
     } else {
       cudaGetLastError();

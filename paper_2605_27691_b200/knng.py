@@ -926,19 +926,29 @@ class RankBuildResult(DistBuildResult):
 
 def build_distributed_rank(x, cfg: RefineConfig, rank: int, world_size: int,
                            allgather=None, device: Optional[int] = None,
-                           metric: str = "l2") -> RankBuildResult:
+                           metric: str = "l2", out=None) -> RankBuildResult:
     """One rank of build_distributed (refine.cpp:504-586) in this process, for
     one process per GPU.  Collective over `allgather(bytes_in, nbytes) ->
     bytes_out` (default: torch_allgather() on the default group).  Every rank
     passes the same full dataset; returns the rank's rows (external ids) and
-    their external row ids (graph.ids[i] is the neighbor list of row rows[i])."""
+    their external row ids (graph.ids[i] is the neighbor list of row rows[i]).
+    `out`: (ids u32 [cap, k], dists f32 [cap, k], rows u32 [cap]) on x's side,
+    cap = ceil(n / world_size) -- e.g. pinned host buffers reused across calls."""
     x = _as_rows(x)
     n = x.shape[0]
     k = cfg.k
     cap = -(-n // world_size)
-    out_i = _empty_like_mem(x, (cap, k), np.uint32)
-    out_d = _empty_like_mem(x, (cap, k), np.float32)
-    out_r = _empty_like_mem(x, (cap,), np.uint32)
+    if out is None:
+        out_i = _empty_like_mem(x, (cap, k), np.uint32)
+        out_d = _empty_like_mem(x, (cap, k), np.float32)
+        out_r = _empty_like_mem(x, (cap,), np.uint32)
+    else:
+        out_i, out_d, out_r = out
+        for a, shape, isz in ((out_i, (cap, k), 4), (out_d, (cap, k), 4), (out_r, (cap,), 4)):
+            if tuple(a.shape) != shape or _mem(a) != _mem(x) or _itemsize(a) != isz or \
+                    not _is_contiguous(a):
+                raise InvalidArgument("build_distributed_rank: out must be contiguous "
+                                      "[cap, k] / [cap, k] / [cap] on x's side")
     ag = allgather or torch_allgather()
     err = []
 
