@@ -110,6 +110,15 @@ def test_nn_descent_out_validation(knng):
             knng.nn_descent(x, k=3, out=g)
 
 
+def test_build_distributed_rank_out_validation(knng):
+    # build_distributed_rank(out=...) checks the caller's buffers first
+    x = np.zeros((10, 4), np.float32)
+    cfg = knng.RefineConfig(ranks=2, groups=2, k=3)
+    bad = (np.zeros((5, 2), np.uint32), np.zeros((5, 3), np.float32), np.zeros(5, np.uint32))
+    with pytest.raises(knng.InvalidArgument):
+        knng.build_distributed_rank(x, cfg, 0, 2, allgather=lambda b, n: b, out=bad)
+
+
 def test_cpp_dropin_compiles(knng):
     """include/knng_b200.hpp (the reference's C++ API over the C-ABI) builds
     and links against libknng_b200.so; tests/cpp/dropin_test.cpp restates
