@@ -569,25 +569,26 @@ def test_reverse_lists_hub_segment(knng):
 
 
 @pytest.mark.gpu
-def test_ann_search_locality_order_is_invisible(knng, monkeypatch):
+@pytest.mark.parametrize("metric", ["l2", "cosine"])
+def test_ann_search_locality_order_is_invisible(knng, monkeypatch, metric):
     # >= 65536 queries run in a Morton processing order (search.cu); every
     # query's result (its entry points are seeded by its index) must equal the
     # one the given order produces (KNNG_SEARCH_ORDER=0)
     x = knng.gen_random_dataset(30000, 16, "clustered", 7, 40)
-    g = knng.nn_descent(x, k=16, seed=3)
-    sg = knng.optimize_graph(g, x, 16)
+    g = knng.nn_descent(x, k=16, seed=3, metric=metric)
+    sg = knng.optimize_graph(g, x, 16, metric=metric)
     q = knng.gen_random_dataset(70000, 16, "clustered", 8, 40)
     p = knng.SearchParams(10, 48, 16, 0, 5)
-    ordered = knng.ann_search(q, sg, x, p, diagnostics=True)
+    ordered = knng.ann_search(q, sg, x, p, diagnostics=True, metric=metric)
     monkeypatch.setenv("KNNG_SEARCH_ORDER", "0")
-    given = knng.ann_search(q, sg, x, p, diagnostics=True)
+    given = knng.ann_search(q, sg, x, p, diagnostics=True, metric=metric)
     assert np.array_equal(ordered.ids, given.ids)
     assert np.array_equal(bits(ordered.dists), bits(given.dists))
     assert np.array_equal(ordered.hops, given.hops)
     assert np.array_equal(ordered.scored, given.scored)
 
 
-@pytest.mark.parametrize("kind", ["f32", "u8_ties"])
+@pytest.mark.parametrize("kind", ["f32", "u8_ties", "cosine"])
 def test_nn_descent_renumbered_build(knng, oracle, monkeypatch, kind):
     """From 2^17 points nn_descent builds on a Morton renumbering of the rows
     (nndescent.cu nn_descent_device) and maps the graph back: rows in the
@@ -595,23 +596,30 @@ def test_nn_descent_renumbered_build(knng, oracle, monkeypatch, kind):
     (u8_ties: a coarse u8 grid where most rows hold ties), exact distances,
     deterministic, and the recall of the plain build."""
     n = 160000
-    if kind == "f32":
+    metric = "cosine" if kind == "cosine" else "l2"
+    if kind in ("f32", "cosine"):
         x = knng.gen_random_dataset(n, 24, "clustered", 11, 64)
     else:
         x = np.random.default_rng(5).integers(0, 6, size=(n, 6)).astype(np.uint8)
-    a = knng.nn_descent(x, k=16, seed=4)
-    b = knng.nn_descent(x, k=16, seed=4)
+    a = knng.nn_descent(x, k=16, seed=4, metric=metric)
+    b = knng.nn_descent(x, k=16, seed=4, metric=metric)
     assert np.array_equal(a.ids, b.ids) and np.array_equal(bits(a.dists), bits(b.dists))
     assert oracle.check_invariants(a.ids, a.dists) == 0
     xf = x.astype(np.float32)
     rng = np.random.default_rng(2)
     rows = rng.integers(0, n, 3000)
     cols = rng.integers(0, 16, 3000)
-    ref = np.array([oracle.l2(xf[r], xf[a.ids[r, c]]) for r, c in zip(rows, cols)], np.float32)
+    dfun = oracle.cosine if kind == "cosine" else oracle.l2
+    ref = np.array([dfun(xf[r], xf[a.ids[r, c]]) for r, c in zip(rows, cols)], np.float32)
     assert np.array_equal(bits(a.dists[rows, cols]), bits(ref))
     monkeypatch.setenv("KNNG_NND_RENUMBER", "0")
-    plain = knng.nn_descent(x, k=16, seed=4)
-    if kind == "f32":
+    plain = knng.nn_descent(x, k=16, seed=4, metric=metric)
+    if kind == "cosine":
+        sample = np.arange(0, n, 97, dtype=np.uint64)
+        gt, _ = knng.brute_force_knng(x, 10, rows=sample, metric="cosine")
+        s = sample.astype(np.int64)
+        assert recall(a.ids[s], gt) >= recall(plain.ids[s], gt) - 0.005
+    elif kind == "f32":
         sample = np.arange(0, n, 97, dtype=np.uint64)
         gt, _ = knng.brute_force_knng(x, 10, rows=sample)
         s = sample.astype(np.int64)
