@@ -93,9 +93,15 @@ __global__ __launch_bounds__(256) void k_join_lists(u64 n, u32 k, u32 B, int RMA
                                                     u32* __restrict__ L_ids,
                                                     u32* __restrict__ L_cnt) {
   __shared__ u32 s_list[8][128];
+  // per-warp membership hash of the list so far (<= 128 of 256 slots used):
+  // a candidate is checked in O(1) probes instead of against every entry
+  constexpr u32 kHash = 256;
+  __shared__ u32 s_hash[8][kHash];
   const unsigned lane = lane_id(), w = threadIdx.x >> 5;
   u32* lst = s_list[w];
+  u32* hs = s_hash[w];
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  auto slot_of = [](u32 c) { return (c * 0x9E3779B1u) >> 24; };  // top 8 bits
   for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + w; p < n; p += warps) {
     // no new entry: the point has no new x new / new x old pair (:157-171);
     // an empty descriptor keeps the join from gathering its old list at all
@@ -103,6 +109,8 @@ __global__ __launch_bounds__(256) void k_join_lists(u64 n, u32 k, u32 B, int RMA
       if (lane == 0) L_cnt[p] = 0;
       continue;
     }
+    for (u32 t = lane; t < kHash; t += 32) hs[t] = kNone;
+    __syncwarp();
     int cnt = 0, nn = 0;
     for (int src = 0; src < 4; ++src) {
       const u32* base = src == 0 ? nf + p * B : src == 1 ? nr + p * B : src == 2 ? of + p * k
@@ -113,9 +121,23 @@ __global__ __launch_bounds__(256) void k_join_lists(u64 n, u32 k, u32 B, int RMA
         const u32 c = valid ? base[b0 + lane] : kNone;
         const unsigned m = __match_any_sync(kFull, c);
         bool keep = valid && (__ffs(m) - 1 == (int)lane);
-        for (int t = 0; t < cnt && keep; ++t) keep = lst[t] != c;
+        if (keep) {
+          for (u32 h = slot_of(c);; h = (h + 1) & (kHash - 1)) {
+            const u32 v = hs[h];
+            if (v == c) {
+              keep = false;
+              break;
+            }
+            if (v == kNone) break;
+          }
+        }
         const unsigned kb = __ballot_sync(kFull, keep);
-        if (keep) lst[cnt + __popc(kb & lanemask_lt())] = c;
+        if (keep) {
+          lst[cnt + __popc(kb & lanemask_lt())] = c;
+          // kept candidates are distinct: claim the first free slot
+          for (u32 h = slot_of(c);; h = (h + 1) & (kHash - 1))
+            if (atomicCAS(&hs[h], kNone, c) == kNone) break;
+        }
         cnt += __popc(kb);
         __syncwarp();
       }

@@ -461,9 +461,9 @@ __global__ __launch_bounds__(256) void k_rev_select_rank(u64 n, u32 B, u64 iter_
       drawn += warp_sample_distinct(rs, drawn, len, B, sp);
       if (len <= 32) {
         // ascending sort across the warp, then pick ranks
-        const u64 x = lane < len ? (u64)seg[lane] : ~0ull;
-        const u32 sorted = (u32)warp_sort32(x);
-        const u32 pick = __shfl_sync(kFull, sorted, lane < B ? sp[lane] : 0);
+        u32 v[1] = {lane < len ? seg[lane] : 0xffffffffu};
+        warp_sort_regs<1>(v, lane);
+        const u32 pick = warp_pick_regs<1>(v, lane < B ? sp[lane] : 0);
         if (lane < B) out[lane] = pick;
       } else if (len <= 64) {
         u32 v[2];
