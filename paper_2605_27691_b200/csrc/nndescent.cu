@@ -849,6 +849,39 @@ __global__ __launch_bounds__(256) void k_apply(u64 n, u32 k, u32 S, u64* __restr
     atomicAdd(reinterpret_cast<unsigned long long*>(counters + kCntAccepted), acc_total);
 }
 
+// Filter refresh between join slices of a dense iteration: worst[p] =
+// min(worst[p], just above the k-th smallest key in p's buckets).  Bucket
+// keys only decrease (a bucket keeps its W smallest distinct keys), and every
+// bucket key ends up in row U buckets -- a key equal to a row entry IS that
+// entry -- so at the end row U buckets still holds >= k keys at or below the
+// bound: a later offer above it can neither enter the final top-k nor, being
+// larger than every key it could displace that matters, change which keys
+// below it the buckets keep.  k_apply's result is unchanged; the offers
+// shrink.  (Exact keys only: not with the tensor-core join's lower bounds.)
+__global__ __launch_bounds__(256) void k_bucket_bound(u64 n, u32 k, u32 S,
+                                                      float* __restrict__ worst,
+                                                      const u64* __restrict__ slots) {
+  const unsigned lane = lane_id();
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 p = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); p < n; p += warps) {
+    const u64* sl = slots + p * S;
+    const u64 c0 = lane < S ? sl[lane] : kEmptyKey;
+    const u64 c1 = 32 + lane < S ? sl[32 + lane] : kEmptyKey;
+    const unsigned full = __ballot_sync(kFull, c0 != kEmptyKey);
+    const unsigned full1 = __ballot_sync(kFull, c1 != kEmptyKey);
+    if ((u32)(__popc(full) + __popc(full1)) < k) continue;  // fewer than k keys: no bound
+    const u64 a = warp_sort_asc(c0, lane);
+    const u64 b = warp_sort_asc(c1, lane);
+    const u64 br = shfl64(b, 31 - lane);
+    const u64 cs = warp_merge_asc(a < br ? a : br, lane);
+    const u64 kth = shfl64(cs, k - 1);
+    if (lane == 0) {
+      const float w = nextafterf(key_dist(kth), INFINITY);
+      if (w < worst[p]) worst[p] = w;
+    }
+  }
+}
+
 // More than 64 buffered slots per point (candidate_capacity > 64): the same
 // semantics, knn_insert one candidate at a time over 32-slot chunks.
 __global__ __launch_bounds__(256) void k_apply_wide(u64 n, u32 k, u32 S, u64* __restrict__ keys,
@@ -1274,6 +1307,9 @@ void nn_descent_core(Runner& r, const DevRows& ds, const NndParams& p, uint64_t*
     ~EvGuard() { cudaEventDestroy(e); }
   } iter_done_guard{iter_done};
   u64 prev_offers = ~0ull;  // offers queued by the previous iteration
+  // KNNG_BOUND_SLICES (1 = off): join slices of a dense iteration
+  u64 bound_slices = 4;
+  if (const char* v = std::getenv("KNNG_BOUND_SLICES")) bound_slices = std::max(1, std::atoi(v));
   for (u64 iter = 0; iter < p.max_iters; ++iter) {
     const bool use_touched = S <= 64 && prev_offers < 4 * n;
     zero_counters();
@@ -1290,10 +1326,20 @@ void nn_descent_core(Runner& r, const DevRows& ds, const NndParams& p, uint64_t*
     // kernels bound themselves by it (no host round trip mid-iteration; the
     // slices past the count exit at once)
     jl.n_live = act_off_p + n;
-    const u64 nslices = ceil_div<u64>(n, slice);
+    // iteration 0 (random rows: nearly every pair passes the row filter)
+    // runs the join in bound_slices slices with k_bucket_bound tightening
+    // the filter between them (later dense iterations gain too little to pay
+    // for the extra passes: C2 offers 216M -> 154M in iteration 2)
+    const bool bound = !use_tc && S <= 64 && bound_slices > 1 && iter == 0;
+    u64 it_slice = slice;
+    if (bound) {
+      const u64 want = ceil_div<u64>(ceil_div<u64>(n, bound_slices), (u64)kJoinChunk) * kJoinChunk;
+      if (want < it_slice) it_slice = want;
+    }
+    const u64 nslices = ceil_div<u64>(n, it_slice);
     for (u64 si = 0; si < nslices; ++si) {
-      jl.p_lo = si * slice;
-      jl.p_hi = std::min<u64>(n, jl.p_lo + slice);
+      jl.p_lo = si * it_slice;
+      jl.p_hi = std::min<u64>(n, jl.p_lo + it_slice);
       KNNG_CUDA(cudaMemsetAsync(chunk_ctr_p, 0, sizeof(u32), r.stream));
       tm.tick(kStLists);
       if (use_tc) {
@@ -1308,6 +1354,12 @@ void nn_descent_core(Runner& r, const DevRows& ds, const NndParams& p, uint64_t*
                    counters_p, jl.p_lo, jl.n_live, n, use_touched ? touched_p : nullptr);
       tm.tick(kStOffer);
       launches += 2;
+      if (bound && si + 1 < nslices) {
+        k_bucket_bound<<<warp_grid(r, n), 256, 0, r.stream>>>(n, k, S, worst_p, slots_p);
+        KNNG_LAUNCH_CHECK();
+        ++launches;
+        tm.tick(kStOffer);
+      }
     }
     if (S <= 64)
       k_apply<<<warp_grid(r, (n + 31) / 32), 256, 0, r.stream>>>(
