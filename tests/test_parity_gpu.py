@@ -661,3 +661,18 @@ def test_join_pair_layout_bitexact(knng, monkeypatch, n, d, metric):
     monkeypatch.setenv("KNNG_JOIN_PAIR", "0")
     b = knng.nn_descent(x, k=16, seed=2, metric=metric)
     assert np.array_equal(a.ids, b.ids) and np.array_equal(bits(a.dists), bits(b.dists))
+
+
+def test_nn_descent_wide_candidate_buffer(knng, oracle):
+    # candidate_capacity > 64 (128 slots per point) takes k_apply_wide:
+    # invariants, exact distances, determinism, recall of the default build
+    x = knng.gen_random_dataset(20000, 16, "clustered", 9, 20)
+    a = knng.nn_descent(x, k=16, seed=2, candidate_capacity=128)
+    b = knng.nn_descent(x, k=16, seed=2, candidate_capacity=128)
+    assert np.array_equal(a.ids, b.ids) and np.array_equal(bits(a.dists), bits(b.dists))
+    assert oracle.check_invariants(a.ids, a.dists) == 0
+    rows = np.arange(0, 20000, 13, dtype=np.uint64)
+    gt, _ = knng.brute_force_knng(x, 10, rows=rows)
+    s = rows.astype(np.int64)
+    base = knng.nn_descent(x, k=16, seed=2)
+    assert recall(a.ids[s], gt) >= recall(base.ids[s], gt) - 0.005
