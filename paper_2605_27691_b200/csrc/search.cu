@@ -615,9 +615,20 @@ SearchShape search_shape(int d, u32 width, u64 entries, bool exact) {
     s.cache = 1;
     s.vis_slots = slots;
   }
-  s.vis_limit = s.vis_slots * 3 / 4;
   s.pipe = env_u32("KNNG_SEARCH_PIPE", 0) != 0 && (u32)d > s.dch;
   s.smem = search_layout(d, width, s.vis_slots, s.stride * (s.pipe ? 2 : 1)).total;
+  // cache mode: a larger filter forgets fewer visited ids (cache mode scores
+  // ~14% more rows than the exact set at C4) -- doubled while the CTA still
+  // fits KNNG_SEARCH_MINB per SM (d = 96: 2M queries 0.495 -> 0.490 s)
+  if (s.cache && !getenv("KNNG_SEARCH_VIS") && s.vis_slots < 8192) {
+    const size_t bigger =
+        search_layout(d, width, 2 * s.vis_slots, s.stride * (s.pipe ? 2 : 1)).total;
+    if ((bigger + 1024) * KNNG_SEARCH_MINB <= 228 * 1024) {
+      s.vis_slots *= 2;
+      s.smem = bigger;
+    }
+  }
+  s.vis_limit = s.vis_slots * 3 / 4;
   return s;
 }
 
