@@ -19,30 +19,35 @@ namespace {
 constexpr int kAxes = 3;
 constexpr int kBits = 10;
 
-// projections p[i][a] = <x_i, R_a>, and per-axis min / max (as ordered ints)
+// projections p[i][a] = <x_i, R_a>, and per-axis min / max (as ordered ints):
+// warp per row, lanes over the dims (coalesced row reads), shuffle-reduced
+// (a fixed order: the projection only has to be deterministic)
 __global__ void k_project(const float* __restrict__ X, u64 n, int d, const float* __restrict__ R,
                           float* __restrict__ P, int* __restrict__ mn, int* __restrict__ mx) {
   __shared__ float sR[kAxes * 1024];
   for (int t = threadIdx.x; t < kAxes * d && t < kAxes * 1024; t += blockDim.x) sR[t] = R[t];
   __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
   int lmin[kAxes], lmax[kAxes];
 #pragma unroll
   for (int a = 0; a < kAxes; ++a) {
     lmin[a] = 0x7fffffff;
     lmax[a] = (int)0x80000000;
   }
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (u64)gridDim.x * blockDim.x) {
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 i = (((u64)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
     float acc[kAxes] = {0.f, 0.f, 0.f};
     const float* xr = X + i * (u64)d;
-    for (int j = 0; j < d; ++j) {
+    for (int j = lane; j < d; j += 32) {
       const float v = xr[j];
 #pragma unroll
       for (int a = 0; a < kAxes; ++a) acc[a] = fmaf(v, sR[a * d + j], acc[a]);
     }
 #pragma unroll
     for (int a = 0; a < kAxes; ++a) {
-      P[i * kAxes + a] = acc[a];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], o);
+      if (lane == a) P[i * kAxes + a] = acc[a];
       // float -> order-preserving int
       int b = __float_as_int(acc[a]);
       b = b >= 0 ? b : b ^ 0x7fffffff;
@@ -52,8 +57,10 @@ __global__ void k_project(const float* __restrict__ X, u64 n, int d, const float
   }
 #pragma unroll
   for (int a = 0; a < kAxes; ++a) {
-    atomicMin(mn + a, lmin[a]);
-    atomicMax(mx + a, lmax[a]);
+    if (lane == 0) {
+      atomicMin(mn + a, lmin[a]);
+      atomicMax(mx + a, lmax[a]);
+    }
   }
 }
 
@@ -111,7 +118,8 @@ void locality_order(const Runner& r, const float* X, uint64_t n, int d, uint64_t
   k_dirs<<<ceil_div(kAxes * d, 256), 256, 0, r.stream>>>(seed, kAxes * d, dR.p, mm.p);
   KNNG_LAUNCH_CHECK();
   const unsigned grid = (unsigned)std::min<u64>(ceil_div<u64>(n, 256), (u64)r.num_sms * 8);
-  k_project<<<grid, 256, 0, r.stream>>>(X, n, d, dR.p, P.p, mm.p, mm.p + kAxes);
+  const unsigned pgrid = (unsigned)std::min<u64>(ceil_div<u64>(n, 8), (u64)r.num_sms * 16);
+  k_project<<<pgrid, 256, 0, r.stream>>>(X, n, d, dR.p, P.p, mm.p, mm.p + kAxes);
   KNNG_LAUNCH_CHECK();
   DBuf<u32> code(r, n), tk(r, n), tv(r, n);
   k_morton<<<grid, 256, 0, r.stream>>>(P.p, n, mm.p, mm.p + kAxes, code.p, order);
