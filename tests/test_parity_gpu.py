@@ -614,16 +614,21 @@ def test_nn_descent_renumbered_build(knng, oracle, monkeypatch, kind):
     assert np.array_equal(bits(a.dists[rows, cols]), bits(ref))
     monkeypatch.setenv("KNNG_NND_RENUMBER", "0")
     plain = knng.nn_descent(x, k=16, seed=4, metric=metric)
-    if kind == "cosine":
-        sample = np.arange(0, n, 97, dtype=np.uint64)
-        gt, _ = knng.brute_force_knng(x, 10, rows=sample, metric="cosine")
+    if kind in ("cosine", "f32"):
+        # a renumbered build is another random instance of the algorithm:
+        # compare mean recall over three seeds on 1/11 of the rows (one
+        # instance on 1,650 rows differed by up to 0.006 either way; over
+        # six seeds the renumbered mean was 0.0005 higher)
+        sample = np.arange(0, n, 11, dtype=np.uint64)
+        gt, _ = knng.brute_force_knng(x, 10, rows=sample, metric=metric)
         s = sample.astype(np.int64)
-        assert recall(a.ids[s], gt) >= recall(plain.ids[s], gt) - 0.005
-    elif kind == "f32":
-        sample = np.arange(0, n, 97, dtype=np.uint64)
-        gt, _ = knng.brute_force_knng(x, 10, rows=sample)
-        s = sample.astype(np.int64)
-        assert recall(a.ids[s], gt) >= recall(plain.ids[s], gt) - 0.005
+        ren, pln = [], []
+        for seed in (4, 5, 6):
+            monkeypatch.delenv("KNNG_NND_RENUMBER", raising=False)
+            ren.append(recall(knng.nn_descent(x, k=16, seed=seed, metric=metric).ids[s], gt))
+            monkeypatch.setenv("KNNG_NND_RENUMBER", "0")
+            pln.append(recall(knng.nn_descent(x, k=16, seed=seed, metric=metric).ids[s], gt))
+        assert np.mean(ren) >= np.mean(pln) - 0.005, (ren, pln)
     else:
         # ties everywhere: compare the distance profiles (ids are arbitrary among ties)
         assert abs(float(a.dists.mean()) - float(plain.dists.mean())) < 0.02 * float(plain.dists.mean())
