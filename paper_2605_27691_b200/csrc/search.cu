@@ -297,7 +297,8 @@ __device__ __forceinline__ u64 score_batch(const SearchArgs& a, const float* __r
 // reach it); unmoved entries are not stored.
 __device__ __forceinline__ void beam_merge(u64 c, u64* __restrict__ beam,
                                            unsigned char* __restrict__ flag,
-                                           u32* __restrict__ s_clo, u32& bs, u32 width) {
+                                           u32* __restrict__ s_clo, u32& bs, u32 width,
+                                           u32& low_insert) {
   const unsigned lane = lane_id();
   if (bs == width && c != kEmptyKey && c >= beam[width - 1]) c = kEmptyKey;
   if (!__any_sync(kFull, c != kEmptyKey)) return;
@@ -350,6 +351,7 @@ __device__ __forceinline__ void beam_merge(u64 c, u64* __restrict__ beam,
   if (keep) s_clo[__popc(kb & lanemask_lt())] = clo;
   // entries before the first insertion point keep their slots
   const u32 first = __reduce_min_sync(kFull, keep ? clo : 0xffffffffu);
+  low_insert = min(low_insert, first);
   __syncwarp();
   for (int t = (int)((bs + 31) >> 5) - 1; t >= (int)(first >> 5); --t) {
     const u32 i = lane + 32u * (u32)t;
@@ -447,6 +449,7 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
     Visited vis{s_vis, a.vis_slots - 1, a.gtable ? a.gtable + (u64)blockIdx.x * a.gcap : nullptr,
                 a.gcap, (u32)(q + 1), false, 0};
     u32 bs = 0;
+    u32 low_insert = 0;  // lowest beam position a merge inserted at (scan hint)
     u32 scored = 0;
 
     // exact mode: spill before the batch can overfill the smem table
@@ -460,7 +463,7 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
     };
     auto score_and_merge = [&](u32 id, bool take) {
       const u64 c = score_batch<kCos>(a, s_q, s_stage, s_ptr, id, take, qnorm);
-      beam_merge(c, s_beam, s_flag, s_clo, bs, W);
+      beam_merge(c, s_beam, s_flag, s_clo, bs, W, low_insert);
     };
     // SearchDiagnostics::scored_ids (annsearch.hpp:36-41): every scored id in
     // scoring order (exact mode only: no id is ever scored twice)
@@ -510,10 +513,14 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
 
     // expansion loop (annsearch.cpp:103-120)
     u32 hops = 0;
+    u32 scan_from = 0;  // entries before it are expanded and unmoved
     while (hops < a.max_hops) {
-      // first unexpanded beam entry (annsearch.cpp:104-108)
+      // first unexpanded beam entry (annsearch.cpp:104-108): every entry
+      // before min(last expanded, lowest insertion since) is expanded
       u32 idx = kNoId;
-      for (u32 t = 0; t * 32 < bs; ++t) {
+      const u32 t0 = min(scan_from, low_insert) >> 5;
+      low_insert = 0xffffffffu;
+      for (u32 t = t0; t * 32 < bs; ++t) {
         const u32 i = t * 32 + lane;
         const unsigned m = __ballot_sync(kFull, i < bs && s_flag[i] == 0);
         if (m) {
@@ -522,6 +529,7 @@ __global__ __launch_bounds__(32, KNNG_SEARCH_MINB) void k_search(SearchArgs a) {
         }
       }
       if (idx == kNoId) break;  // every beam entry expanded
+      scan_from = idx;
       const u32 u = key_id(s_beam[idx]);
       __syncwarp();
       if (lane == 0) s_flag[idx] = 1;
