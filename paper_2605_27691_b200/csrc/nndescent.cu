@@ -1,21 +1,31 @@
 // nndescent.cu -- B200 lock-free NN-Descent (north_star item 2).
 //
-// Per iteration (nndescent.cpp:247-257):
+// nn_descent_device builds on a Morton renumbering of the points (locality.cu)
+// from 2^17 points on and maps the graph back.  Per iteration
+// (nndescent.cpp:247-257):
 //   k_sample_fwd   warp per point: forward new/old samples, exactly the
 //                  reference's sampling stream (nndescent.cpp:80-104)
-//   scan + k_make_pairs + radix sort + k_rev_select: the serial transpose (:108-113) as a
-//                  counting sort; each reverse list is ranked in ascending
-//                  source order and sampled with the reference's rng stream
-//                  (:114-127), so the sampled lists equal the reference's.
-//   k_join         CTA per point: dedup'd new/old lists (:135-153), feature
-//                  rows staged in smem with cp.async (16 B), 4x4 register
-//                  micro-tiles of exact-order distances, offers (:157-197)
-//                  resolved by 64-bit packed (dist,id) atomicMin cascades
-//                  into hashed 4-way candidate buckets that keep the 4
-//                  smallest distinct keys -- lock-free and order-independent,
-//                  so the build is deterministic regardless of scheduling.
-//   k_apply        warp per point: knn_insert of every surviving slot in slot
-//                  order (:199-223), gross accepted count, worst refresh.
+//   reverse lists  the serial transpose (:108-113): sources scattered into
+//                  their targets' segments (k_rev_scatter; old entries only
+//                  for targets that join, through a joins bitmap), a segment
+//                  longer than the bound ranked in ascending source order
+//                  (k_rev_select_rank / _long) and sampled with the
+//                  reference's rng stream (:114-127) -- the picks equal the
+//                  sorted path's (the stable radix sort + k_rev_select path
+//                  serves sample_neighbors and KNNG_REV_SORT=1)
+//   k_join         persistent CTAs over batches of points (join.cu): dedup'd
+//                  new/old lists (:135-153), feature rows staged in smem with
+//                  cp.async, 4x4 register micro-tiles of exact-order
+//                  distances, offers (:157-197) resolved by 64-bit packed
+//                  (dist,id) atomicMin cascades into hashed 4-way candidate
+//                  buckets that keep the 4 smallest distinct keys -- lock-free
+//                  and order-independent, so the build is deterministic;
+//                  iteration 0 runs in slices with an exact bucket bound on
+//                  the offer filter between them (k_bucket_bound)
+//   k_apply        warp per point: the row becomes the k smallest of
+//                  (row U candidates) with knn_insert semantics (:199-223),
+//                  the candidates taken in ascending key order (accepted =
+//                  kept), worst refreshed; only touched points once sparse.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>

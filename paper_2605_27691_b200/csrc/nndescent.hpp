@@ -29,7 +29,7 @@ struct NndParams {
 enum NndStage : int { kStInit = 0, kStSample, kStLists, kStJoin, kStOffer, kStApply, kStSync };
 
 enum NndCounter : int {
-  kCntAccepted = 0,    // gross successful knn_insert calls (nndescent.cpp:213)
+  kCntAccepted = 0,    // accepted inserts, ascending-key order = entries kept (nndescent.cpp:213)
   kCntPairs = 1,       // sigma evaluations (JoinCounts::pairs)
   kCntStagedRows = 2,  // feature rows staged into smem by the join (algorithmic bytes)
   kCntOffers = 3,      // offers passing the worst filter (atomicMin issued)
